@@ -1,0 +1,190 @@
+/* maxwell_dd.h -- C ABI of the B200-native two-level Schwarz / GenEO PCG solver
+ * for the lowest-order Nédélec discretisation of the positive Maxwell problem
+ *
+ *     curl(mu^{-1} curl E) + gamma eps E = f  in Omega,   E x n = 0 on the Dirichlet part
+ *
+ * (eq. 1.1; discrete system A U := (K + gamma M) U = f, eq. 1.5).
+ *
+ * The library owns its device memory; every pointer argument is either a HOST
+ * pointer or a DEVICE pointer as stated per argument.  All functions return 0 on
+ * success and a nonzero MDD_ERR_* code on failure; the message is then available
+ * from mdd_last_error() (thread-local, valid until the next call).  No function
+ * ever falls back to a CPU computation: a missing device or a CUDA error is an
+ * error.  Indices are 0-based.
+ *
+ * Numbering contract (shared with any checker):
+ *   node id     = i + (nx+1)*(j + (ny+1)*k),       0 <= i <= nx, ...
+ *   cube id     = ci + nx*(cj + ny*ck);  tet id = 6*cube + s, s indexing the Kuhn
+ *                 paths v -> v+e_a -> v+e_a+e_b -> v+(1,1,1) for
+ *                 (a,b) in (x,y) (x,z) (y,x) (y,z) (z,x) (z,y)
+ *   edges       = pairs (tail, head) of node ids, tail < head, numbered in
+ *                 lexicographic (tail, head) order; orientation tail -> head
+ *   free dofs   = non-Dirichlet edges, same order; free nodes likewise
+ *   Dirichlet   = edges / nodes of boundary triangles on the box faces
+ *                 (MDD_DIRICHLET_OUTER), on every boundary incl. hole walls
+ *                 (MDD_DIRICHLET_ALL) or none (MDD_DIRICHLET_NONE)
+ *   subdomain s = si + px*(sj + py*sk); it owns the cube box
+ *                 [si*nx/px, (si+1)*nx/px) x ... and Omega_s adds `overlap`
+ *                 cube layers around it (§4 "One layer of elements is
+ *                 added in each direction"); N_s = free edges of its tets, increasing.
+ */
+#ifndef MAXWELL_DD_H
+#define MAXWELL_DD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDD_OK 0
+#define MDD_ERR_CUDA 1      /* CUDA / cuSOLVER / cuBLAS failure or no device       */
+#define MDD_ERR_ARG 2       /* invalid argument (sizes, modes, divisibility)        */
+#define MDD_ERR_NOTPD 3     /* a matrix that must be SPD had a nonpositive pivot    */
+#define MDD_ERR_NOCONV 4    /* PCG hit maxit (the result is still returned)          */
+#define MDD_ERR_INTERNAL 5  /* broken internal invariant                             */
+#define MDD_ERR_BREAKDOWN 6 /* PCG breakdown (p^T A p <= 0)                          */
+
+#define MDD_DIRICHLET_OUTER 0
+#define MDD_DIRICHLET_ALL 1
+#define MDD_DIRICHLET_NONE 2
+
+#define MDD_COARSE_NONE 0   /* one-level AS, eq. (2.3)                              */
+#define MDD_COARSE_SNK 1    /* split near-kernel, Def. 2.3 (+ GenEO, GEVP 3.5)      */
+#define MDD_COARSE_NK 2     /* global near-kernel G = C (§4 "AS-NK") (+ GenEO)      */
+
+#define MDD_VARIANT_AS2 0       /* M_AS,2 = Q + (I - QA) M_AS (I - AQ), eq. (2.4)   */
+#define MDD_VARIANT_ADDITIVE 1  /* M_AS + Q (north_star's written sum, D_i dropped) */
+#define MDD_VARIANT_AS1 2       /* M_AS only                                        */
+
+typedef struct mdd_solver* mdd_handle;
+
+typedef struct {
+  int nx, ny, nz;              /* cube grid                                           */
+  double h;                    /* cube edge length                                    */
+  const uint8_t* cube_mask;    /* HOST, nx*ny*nz (1 = cube present) or NULL = all     */
+  int dirichlet;               /* MDD_DIRICHLET_*                                     */
+  const double* mu_inv;        /* HOST, 6*nx*ny*nz per tet (indexed by tet id), > 0   */
+  const double* eps;           /* HOST, 6*nx*ny*nz per tet, > 0                       */
+  double gamma;                /* > 0                                                 */
+  int px, py, pz;              /* subdomain boxes per axis; must divide nx, ny, nz    */
+  int overlap;                 /* cube layers added around each box, >= 0            */
+  double coarse_threshold;     /* GenEO keeps eigenpairs of GEVP 3.5 with
+                                  lambda > tau = 1/coarse_threshold; <= 0: no GenEO   */
+  int coarse_kind;             /* MDD_COARSE_*                                        */
+  int variant;                 /* MDD_VARIANT_*                                       */
+  int device;                  /* CUDA device ordinal                                 */
+  int reserved[8];             /* must be zero                                        */
+} mdd_setup_desc;
+
+/* Build everything the solve phase needs (§2-§3): mesh + numbering,
+ * assembly of K, M, A (device), overlapping decomposition, R_i, D_i, local
+ * supernodal LDL^T factors of A_i = R_i A R_i^T (device), the coarse space Z
+ * (SNK Def. 2.3 or NK, plus GenEO columns of GEVP 3.5 solved on the device) and
+ * the LDL^T factor of E = Z^T A Z.  Inputs are host pointers, copied; the caller
+ * keeps ownership.  *out receives a handle owned by the caller (mdd_destroy). */
+int mdd_setup(const mdd_setup_desc* desc, mdd_handle* out);
+
+void mdd_destroy(mdd_handle h);
+
+/* Preconditioned CG (x0 = 0) on A x = f with the configured preconditioner,
+ * stopping at ||r_k||_2 <= tol ||f||_2 or maxit.  f, x: DEVICE pointers to n
+ * doubles (n = free dofs, MDD_INFO_N).  *iters, *relres: HOST outputs.  Runs on
+ * the handle's stream and synchronises it before returning. */
+int mdd_solve(mdd_handle h, const double* f, double* x, double tol, int maxit, int* iters,
+              double* relres);
+
+/* Same, with HOST f and x; the host<->device copies are part of the call. */
+int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int maxit,
+                   int* iters, double* relres);
+
+/* z = M^{-1} r for the configured variant (eq. 2.3 / 2.4).  DEVICE pointers. */
+int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z);
+/* y = A x (CSR SpMV).  DEVICE pointers. */
+int mdd_apply_operator(mdd_handle h, const double* x, double* y);
+/* z = sum_i R_i^T A_i^{-1} R_i r (eq. 2.3).  DEVICE pointers. */
+int mdd_apply_local(mdd_handle h, const double* r, double* z);
+/* y = Z E^{-1} Z^T v (coarse correction Q).  DEVICE pointers. */
+int mdd_apply_coarse(mdd_handle h, const double* v, double* y);
+
+/* Integer / scalar facts about the handle (HOST array out[0..MDD_INFO_COUNT)). */
+enum {
+  MDD_INFO_N = 0,           /* free edge dofs n                        */
+  MDD_INFO_NEDGES,          /* all edges                               */
+  MDD_INFO_NFREE_NODES,     /* free nodes (columns of C)               */
+  MDD_INFO_NSUB,            /* subdomains                              */
+  MDD_INFO_NNZ_A,           /* nonzeros of A                           */
+  MDD_INFO_NLOC,            /* sum_i n_i                               */
+  MDD_INFO_GRAD_CANDIDATES, /* gradient candidate columns (SNK family) */
+  MDD_INFO_GRAD_RANK,       /* dim V_G kept                            */
+  MDD_INFO_NGENEO,          /* GenEO columns                           */
+  MDD_INFO_N0,              /* coarse dimension                        */
+  MDD_INFO_LOCAL_FACTOR_NNZ,/* stored entries of the local factors     */
+  MDD_INFO_COARSE_FACTOR_NNZ,
+  MDD_INFO_LOCAL_SUPERNODES,
+  MDD_INFO_LOCAL_LEVELS,
+  MDD_INFO_COARSE_SUPERNODES,
+  MDD_INFO_COARSE_LEVELS,
+  MDD_INFO_NNZ_Z,
+  MDD_INFO_KERNELS_PER_ITER, /* kernel launches per PCG iteration       */
+  MDD_INFO_COUNT
+};
+int mdd_info(mdd_handle h, int64_t* out, int count);
+
+/* Copy an internal integer array to HOST memory (int64 elements).  *len gets the
+ * full length; at most cap elements are written (out may be NULL to query). */
+enum {
+  MDD_ARR_EDGE_TAIL = 0,    /* all edges                                 */
+  MDD_ARR_EDGE_HEAD,
+  MDD_ARR_FREE_EDGES,       /* free dof -> edge index                    */
+  MDD_ARR_FREE_NODES,       /* free node -> node id                      */
+  MDD_ARR_A_PTR,            /* CSR of A (free dofs), n+1                 */
+  MDD_ARR_A_IDX,
+  MDD_ARR_SUB_PTR,          /* nsub+1 offsets into MDD_ARR_SUB_DOFS       */
+  MDD_ARR_SUB_DOFS,         /* concatenated N_i                           */
+  MDD_ARR_GRAD_NODES_PTR,   /* nsub+1 offsets into MDD_ARR_GRAD_NODES     */
+  MDD_ARR_GRAD_NODES,       /* per subdomain: free-node columns of G_i    */
+  MDD_ARR_GENEO_COUNT,      /* nsub: GenEO vectors kept per subdomain     */
+  MDD_ARR_COUNT
+};
+int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len);
+
+/* Host-only topology query (no device needed): builds the mesh numbering, the
+ * pattern of A, the decomposition and the G_i columns for `desc` (coefficients
+ * are ignored and may be NULL) and copies array `which` (MDD_ARR_*, except
+ * MDD_ARR_GENEO_COUNT) to HOST memory as for mdd_get_int_array. */
+int mdd_topology_int_array(const mdd_setup_desc* desc, int which, int64_t* out, int64_t cap,
+                           int64_t* len);
+
+/* Copy an internal double array to HOST memory. */
+enum {
+  MDD_DARR_A_VAL = 0,       /* values of A in MDD_ARR_A_IDX order         */
+  MDD_DARR_K_VAL,           /* K in the same pattern                      */
+  MDD_DARR_M_VAL,           /* M in the same pattern                      */
+  MDD_DARR_GENEO_LAMBDA,    /* kept eigenvalues, subdomain-major          */
+  MDD_DARR_SETUP_TIMES,     /* seconds per setup phase (see mdd_phase_name)*/
+  MDD_DARR_COUNT
+};
+int mdd_get_double_array(mdd_handle h, int which, double* out, int64_t cap, int64_t* len);
+const char* mdd_phase_name(int phase);
+
+/* Per-phase device time of the last mdd_solve with profiling enabled, in ms
+ * (HOST out[0..MDD_PROF_COUNT)), and the number of launches of each phase. */
+enum {
+  MDD_PROF_SPMV = 0,        /* A p (+ dot)                               */
+  MDD_PROF_LOCAL_FWD,       /* forward+diagonal supernodal solves        */
+  MDD_PROF_LOCAL_BWD,       /* backward supernodal solves                */
+  MDD_PROF_COARSE,          /* Z^T, coarse solves, Z                     */
+  MDD_PROF_VECTOR,          /* PCG vector updates, reductions            */
+  MDD_PROF_TOTAL,
+  MDD_PROF_COUNT
+};
+int mdd_set_profiling(mdd_handle h, int enable);
+int mdd_profile(mdd_handle h, double* ms, int64_t* launches, int count);
+
+const char* mdd_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAXWELL_DD_H */

@@ -1,0 +1,947 @@
+// C-ABI entry points and the setup / solve orchestration of maxwell_dd.
+//
+// Setup (§2-§3, timed per phase): host integer work (mesh numbering,
+// patterns, decomposition, symbolic factorisations) and device numeric work
+// (assembly, local multifrontal LDL^T, GenEO GEVPs, coarse Gram / E products and
+// the E factorisation).  Solve (the hot path): PCG whose every step runs in the
+// kernels of kernels.cu.
+#include <cuda_runtime.h>
+#include <cusparse.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+
+#include "../../include/maxwell_dd.h"
+#include "device.h"
+#include "geneo.h"
+#include "topology.h"
+
+using namespace mdd;
+
+namespace {
+thread_local std::string g_err;
+
+enum { PH_MESH = 0, PH_PATTERN, PH_ASSEMBLY, PH_DECOMP, PH_LOCAL_SYMBOLIC, PH_LOCAL_FACTOR,
+       PH_GENEO, PH_GRAD_RANK, PH_COARSE_E, PH_COARSE_FACTOR, PH_COUNT };
+const char* kPhaseNames[PH_COUNT] = {"mesh", "pattern", "assembly", "decomposition",
+                                     "local_symbolic", "local_factor", "geneo_gevp",
+                                     "grad_rank", "coarse_E", "coarse_factor"};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+inline int nblk(int64_t n, int t) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
+
+// --------------------------------------------------- cuSPARSE SpGEMM helper
+struct DevCsr {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  DBuf<int> ptr, idx;
+  DBuf<double> val;
+};
+
+void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s) {
+  CUSPARSE_CHECK(cusparseSetStream(H, s));
+  cusparseSpMatDescr_t a, b, c;
+  CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p,
+                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+  CUSPARSE_CHECK(cusparseCreateCsr(&b, B.rows, B.cols, B.nnz, B.ptr.p, B.idx.p, B.val.p,
+                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+  C.rows = A.rows; C.cols = B.cols;
+  C.ptr.alloc(C.rows + 1);
+  CUSPARSE_CHECK(cusparseCreateCsr(&c, C.rows, C.cols, 0, C.ptr.p, nullptr, nullptr,
+                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+  cusparseSpGEMMDescr_t d;
+  CUSPARSE_CHECK(cusparseSpGEMM_createDescr(&d));
+  double one = 1.0, zero = 0.0;
+  auto op = CUSPARSE_OPERATION_NON_TRANSPOSE;
+  size_t b1 = 0, b2 = 0;
+  CUSPARSE_CHECK(cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                               CUSPARSE_SPGEMM_DEFAULT, d, &b1, nullptr));
+  DBuf<char> w1; w1.alloc(std::max<size_t>(b1, 1));
+  CUSPARSE_CHECK(cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                               CUSPARSE_SPGEMM_DEFAULT, d, &b1, w1.p));
+  CUSPARSE_CHECK(cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                        CUSPARSE_SPGEMM_DEFAULT, d, &b2, nullptr));
+  DBuf<char> w2; w2.alloc(std::max<size_t>(b2, 1));
+  CUSPARSE_CHECK(cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                        CUSPARSE_SPGEMM_DEFAULT, d, &b2, w2.p));
+  int64_t r_, c_, nnz;
+  CUSPARSE_CHECK(cusparseSpMatGetSize(c, &r_, &c_, &nnz));
+  C.nnz = nnz;
+  C.idx.alloc(std::max<int64_t>(nnz, 1));
+  C.val.alloc(std::max<int64_t>(nnz, 1));
+  CUSPARSE_CHECK(cusparseCsrSetPointers(c, C.ptr.p, C.idx.p, C.val.p));
+  CUSPARSE_CHECK(cusparseSpGEMM_copy(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                     CUSPARSE_SPGEMM_DEFAULT, d));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cusparseSpGEMM_destroyDescr(d);
+  cusparseDestroySpMat(a); cusparseDestroySpMat(b); cusparseDestroySpMat(c);
+}
+
+void transpose(cusparseHandle_t H, const DevCsr& A, DevCsr& T, cudaStream_t s) {
+  CUSPARSE_CHECK(cusparseSetStream(H, s));
+  T.rows = A.cols; T.cols = A.rows; T.nnz = A.nnz;
+  T.ptr.alloc(T.rows + 1);
+  T.idx.alloc(std::max<int64_t>(A.nnz, 1));
+  T.val.alloc(std::max<int64_t>(A.nnz, 1));
+  size_t bs = 0;
+  CUSPARSE_CHECK(cusparseCsr2cscEx2_bufferSize(H, A.rows, A.cols, A.nnz, A.val.p, A.ptr.p, A.idx.p,
+                                               T.val.p, T.ptr.p, T.idx.p, CUDA_R_64F,
+                                               CUSPARSE_ACTION_NUMERIC, CUSPARSE_INDEX_BASE_ZERO,
+                                               CUSPARSE_CSR2CSC_ALG1, &bs));
+  DBuf<char> w; w.alloc(std::max<size_t>(bs, 1));
+  CUSPARSE_CHECK(cusparseCsr2cscEx2(H, A.rows, A.cols, A.nnz, A.val.p, A.ptr.p, A.idx.p, T.val.p,
+                                    T.ptr.p, T.idx.p, CUDA_R_64F, CUSPARSE_ACTION_NUMERIC,
+                                    CUSPARSE_INDEX_BASE_ZERO, CUSPARSE_CSR2CSC_ALG1, w.p));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// CSR (int32 pointers) download + sort each row; returns pattern and value slot
+void download_sorted(const DevCsr& C, Csr& pat, std::vector<int64_t>& slot) {
+  std::vector<int> ptr(C.rows + 1), idx(C.nnz);
+  CUDA_CHECK(cudaMemcpy(ptr.data(), C.ptr.p, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  if (C.nnz) CUDA_CHECK(cudaMemcpy(idx.data(), C.idx.p, idx.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  pat.nrows = (int)C.rows; pat.ncols = (int)C.cols;
+  pat.ptr.assign(C.rows + 1, 0);
+  pat.idx.resize(C.nnz);
+  slot.resize(C.nnz);
+  for (int64_t r = 0; r < C.rows; ++r) {
+    std::vector<std::pair<int, int64_t>> row;
+    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) row.push_back({idx[k], k});
+    std::sort(row.begin(), row.end());
+    for (size_t j = 0; j < row.size(); ++j) {
+      pat.idx[ptr[r] + j] = row[j].first;
+      slot[ptr[r] + j] = row[j].second;
+    }
+    pat.ptr[r + 1] = ptr[r + 1];
+  }
+}
+
+}  // namespace
+
+// ======================================================================
+struct mdd_solver {
+  mdd_setup_desc desc;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cusparseHandle_t sp = nullptr;
+  HostMesh mesh;
+  Csr Apat;
+  Decomp dec;
+  std::vector<std::vector<int32_t>> grad_nodes;
+  int n = 0;
+  // A
+  DBuf<int64_t> A_ptr;
+  DBuf<int32_t> A_idx;
+  DBuf<double> A_val, K_val, M_val;
+  DBuf<double> Ke, Me;          // element matrices, kept until the GEVPs are done
+  // local solves
+  DevFactor loc;
+  DBuf<int32_t> gmap;          // local position -> global dof
+  DBuf<int64_t> pro_ptr;       // global dof -> list of local positions
+  DBuf<int32_t> pro_pos;
+  // coarse
+  bool has_coarse = false;
+  DevFactor crs;
+  DBuf<int64_t> Z_ptr, Zt_ptr;  // Z: n x n0 (cols = coarse positions); Zt: n0 x n
+  DBuf<int32_t> Z_idx, Zt_idx;
+  DBuf<double> Z_val, Zt_val;
+  int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0;
+  std::vector<int64_t> geneo_count;
+  std::vector<double> geneo_lambda;
+  // PCG work
+  DBuf<double> x, r, p, q, z, t1, t2, t3, t4, xloc, xc, S, part;
+  DBuf<int> state;
+  int* state_host = nullptr;
+  int nparts = 0;
+  std::vector<double> setup_times;
+  int64_t kernels_per_iter = 0;
+  bool profiling = false;
+  double prof_ms[MDD_PROF_COUNT] = {0};
+  int64_t prof_launch[MDD_PROF_COUNT] = {0};
+  cudaEvent_t ev[16];
+
+  ~mdd_solver() {
+    if (state_host) cudaFreeHost(state_host);
+    if (sp) cusparseDestroy(sp);
+    if (profiling)
+      for (auto& e : ev) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // ------------------------------------------------------------ helpers
+  void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
+            double* out, const double* dotw = nullptr, double* part_ = nullptr) {
+    int warps_per_block = 8;
+    dev::k_spmv<<<nblk(rows, warps_per_block), 32 * warps_per_block, 0, stream>>>(
+        rows, ptr, idx, val, in, out, dotw, part_, state.p);
+  }
+  void applyA(const double* in, double* out) {
+    spmv(A_ptr.p, A_idx.p, A_val.p, n, in, out);
+  }
+  void apply_local(const double* rr, double* zz) {
+    loc.forward(rr, gmap.p, xloc.p, stream);
+    loc.backward(xloc.p, stream);
+    dev::k_prolong<<<nblk(n, 256), 256, 0, stream>>>(n, pro_ptr.p, pro_pos.p, xloc.p, zz);
+  }
+  void apply_coarse(const double* v, double* y) {
+    dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
+                                                                 Zt_val.p, v, xc.p, state.p);
+    crs.forward(nullptr, nullptr, xc.p, stream);
+    crs.backward(xc.p, stream);
+    dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
+                                                                         xc.p, y, state.p);
+  }
+  void apply_prec(const double* rr, double* zz) {
+    int v = desc.variant;
+    if (!has_coarse || v == MDD_VARIANT_AS1) {
+      apply_local(rr, zz);
+      return;
+    }
+    if (v == MDD_VARIANT_ADDITIVE) {
+      apply_local(rr, t4.p);
+      apply_coarse(rr, t1.p);
+      dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, t4.p, 1.0, t1.p, zz, state.p);
+      return;
+    }
+    // eq. (2.4): z = Q r + (I - Q A) M_AS (I - A Q) r
+    apply_coarse(rr, t1.p);                                        // t1 = Q r
+    applyA(t1.p, t2.p);                                            // t2 = A Q r
+    dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, rr, -1.0, t2.p, t3.p, state.p);  // t3 = r - A Q r
+    apply_local(t3.p, t4.p);                                       // t4 = w
+    applyA(t4.p, t2.p);                                            // t2 = A w
+    apply_coarse(t2.p, t3.p);                                      // t3 = Q A w
+    dev::k_combine3<<<nblk(n, 256), 256, 0, stream>>>(n, t1.p, t4.p, t3.p, zz, state.p);
+  }
+  void dot(const double* a, const double* b, int slot) {
+    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p);
+    dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
+  }
+};
+
+namespace {
+
+void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
+  MDD_REQUIRE(d != nullptr, 2, "null descriptor");
+  for (int k = 0; k < 8; ++k) MDD_REQUIRE(d->reserved[k] == 0, 2, "reserved fields must be zero");
+  MDD_REQUIRE(d->gamma > 0, 2, "gamma must be > 0");
+  MDD_REQUIRE(d->mu_inv && d->eps, 2, "coefficients required");
+  MDD_REQUIRE(d->coarse_kind >= 0 && d->coarse_kind <= 2, 2, "bad coarse kind");
+  MDD_REQUIRE(d->variant >= 0 && d->variant <= 2, 2, "bad variant");
+  H->desc = *d;
+  H->desc.cube_mask = nullptr;
+  H->desc.mu_inv = H->desc.eps = nullptr;
+  int ndev = 0;
+  CUDA_CHECK(cudaGetDeviceCount(&ndev));
+  MDD_REQUIRE(ndev > 0, 1, "no CUDA device");
+  CUDA_CHECK(cudaSetDevice(d->device));
+  H->device = d->device;
+  CUDA_CHECK(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+  CUSPARSE_CHECK(cusparseCreate(&H->sp));
+  cudaStream_t s = H->stream;
+  H->setup_times.assign(PH_COUNT, 0.0);
+  const int64_t ncubes = (int64_t)d->nx * d->ny * d->nz;
+  for (int64_t t = 0; t < 6 * ncubes; ++t)
+    MDD_REQUIRE(d->mu_inv[t] > 0 && d->eps[t] > 0 && std::isfinite(d->mu_inv[t]) && std::isfinite(d->eps[t]),
+                2, "coefficients must be positive and finite");
+
+  // ---------------------------------------------------------- mesh
+  double t0 = now_s();
+  build_mesh(H->mesh, d->nx, d->ny, d->nz, d->h, d->cube_mask, d->dirichlet);
+  const HostMesh& m = H->mesh;
+  H->n = m.n();
+  MDD_REQUIRE(H->n > 0, 2, "no free dofs");
+  const int n = H->n;
+  H->setup_times[PH_MESH] = now_s() - t0;
+
+  // ------------------------------------------------------- pattern
+  t0 = now_s();
+  std::vector<int64_t> slot_ptr;
+  std::vector<int32_t> contrib;
+  build_A_pattern(m, H->Apat, slot_ptr, contrib);
+  H->setup_times[PH_PATTERN] = now_s() - t0;
+
+  // ------------------------------------------------------ assembly (device)
+  t0 = now_s();
+  {
+    const int64_t T = m.ntets();
+    DBuf<int64_t> tid, tn, sptr;
+    DBuf<int32_t> ctb;
+    DBuf<double> mu, ep;
+    DBuf<double>& Ke = H->Ke;
+    DBuf<double>& Me = H->Me;
+    tid.upload(m.tet_id);
+    tn.upload(m.tet_nodes);
+    mu.upload(d->mu_inv, 6 * ncubes);
+    ep.upload(d->eps, 6 * ncubes);
+    Ke.alloc(T * 36);
+    Me.alloc(T * 36);
+    dev::k_element_matrices<<<nblk(T, 128), 128, 0, s>>>(T, tid.p, tn.p, m.nx, m.ny, m.h, mu.p, ep.p, Ke.p, Me.p);
+    CUDA_CHECK(cudaGetLastError());
+    sptr.upload(slot_ptr);
+    ctb.upload(contrib);
+    const int64_t nnz = H->Apat.nnz();
+    H->A_val.alloc(nnz); H->K_val.alloc(nnz); H->M_val.alloc(nnz);
+    dev::k_assemble_slots<<<nblk(nnz, 256), 256, 0, s>>>(nnz, sptr.p, ctb.p, Ke.p, Me.p, d->gamma,
+                                                        H->A_val.p, H->K_val.p, H->M_val.p);
+    CUDA_CHECK(cudaGetLastError());
+    H->A_ptr.upload(H->Apat.ptr);
+    H->A_idx.upload(H->Apat.idx);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  H->setup_times[PH_ASSEMBLY] = now_s() - t0;
+
+  // -------------------------------------------------- decomposition
+  t0 = now_s();
+  build_subdomains(m, d->px, d->py, d->pz, d->overlap, H->dec);
+  const int nsub = H->dec.nsub;
+  H->setup_times[PH_DECOMP] = now_s() - t0;
+
+  // ---------------------------------------- local symbolic + numeric factor
+  t0 = now_s();
+  std::vector<Csr> lpat(nsub);
+  std::vector<std::vector<int64_t>> lslot(nsub);
+  std::vector<std::vector<int32_t>> lxyz(nsub);
+  {
+    std::vector<int32_t> g2l(n, -1);
+    for (int i = 0; i < nsub; ++i) {
+      local_pattern(H->Apat, H->dec.sub_dofs[i], g2l, lpat[i], lslot[i]);
+      const auto& D = H->dec.sub_dofs[i];
+      lxyz[i].resize(3 * D.size());
+      for (size_t k = 0; k < D.size(); ++k) edge_xyz2(m, D[k], &lxyz[i][3 * k]);
+    }
+    std::vector<SymSystem> sys(nsub);
+    for (int i = 0; i < nsub; ++i) sys[i] = SymSystem{&lpat[i], lxyz[i].data(), lslot[i].data()};
+    build_factor_plan(H->loc.fp, sys, 64);
+    H->loc.upload();
+    // position -> global dof, global dof -> positions (subdomain order)
+    const FactorPlan& fp = H->loc.fp;
+    std::vector<int32_t> gm(fp.ntot);
+    for (int i = 0; i < nsub; ++i)
+      for (int64_t k = fp.sys_off[i]; k < fp.sys_off[i + 1]; ++k)
+        gm[k] = H->dec.sub_dofs[i][fp.perm[k]];
+    H->gmap.upload(gm);
+    std::vector<int64_t> pp(n + 1, 0);
+    for (int i = 0; i < nsub; ++i)
+      for (int32_t e : H->dec.sub_dofs[i]) pp[e + 1]++;
+    for (int e = 0; e < n; ++e) pp[e + 1] += pp[e];
+    std::vector<int32_t> pos(pp[n]);
+    std::vector<int64_t> cur(pp.begin(), pp.end() - 1);
+    for (int i = 0; i < nsub; ++i)
+      for (size_t k = 0; k < H->dec.sub_dofs[i].size(); ++k)
+        pos[cur[H->dec.sub_dofs[i][k]]++] = fp.iperm_global[fp.sys_off[i] + k];
+    H->pro_ptr.upload(pp);
+    H->pro_pos.upload(pos);
+  }
+  H->setup_times[PH_LOCAL_SYMBOLIC] = now_s() - t0;
+  t0 = now_s();
+  H->loc.factor(H->A_val.p, 0, 0.0, nullptr, s);
+  H->setup_times[PH_LOCAL_FACTOR] = now_s() - t0;
+
+  // --------------------------------------------------------- coarse space
+  H->has_coarse = d->coarse_kind != MDD_COARSE_NONE;
+  H->geneo_count.assign(nsub, 0);
+  if (H->has_coarse) {
+    // gradient nodes of every subdomain (needed by SNK and by the GEVP's xi)
+    H->grad_nodes.resize(nsub);
+    for (int i = 0; i < nsub; ++i) gradient_nodes(m, H->dec.sub_dofs[i], H->grad_nodes[i]);
+    // ---- GenEO columns (device dense GEVPs), local coordinates per subdomain
+    t0 = now_s();
+    std::vector<GeneoBlock> geneo(nsub);
+    if (d->coarse_threshold > 0) {
+      const double tau = 1.0 / d->coarse_threshold;
+      GeneoInputs gin{&m, &H->dec, &lpat, &lslot, H->A_val.p, H->Ke.p, H->Me.p, d->gamma, &H->grad_nodes};
+      geneo_all(gin, tau, geneo, s);
+      for (int i = 0; i < nsub; ++i) {
+        H->geneo_count[i] = geneo[i].k;
+        for (double l : geneo[i].lambda) H->geneo_lambda.push_back(l);
+        H->ngeneo += geneo[i].k;
+      }
+    }
+    H->setup_times[PH_GENEO] = now_s() - t0;
+
+    // ---- gradient candidates: columns (dof, sign) per (subdomain, node)
+    t0 = now_s();
+    struct Cand { int sub; int node; };
+    std::vector<Cand> cand;
+    std::vector<int64_t> cptr(1, 0);
+    std::vector<int32_t> cdof;
+    std::vector<int8_t> csign;
+    // free edges incident to each free node
+    const int nfn = (int)m.free_node.size();
+    std::vector<int64_t> np(nfn + 1, 0);
+    for (int e = 0; e < n; ++e) {
+      int ee = m.free_edge[e];
+      int a = m.node_to_free[m.edge_tail[ee]], b = m.node_to_free[m.edge_head[ee]];
+      if (a >= 0) np[a + 1]++;
+      if (b >= 0) np[b + 1]++;
+    }
+    for (int v = 0; v < nfn; ++v) np[v + 1] += np[v];
+    std::vector<int32_t> nedge(np[nfn]);
+    {
+      std::vector<int64_t> cur(np.begin(), np.end() - 1);
+      for (int e = 0; e < n; ++e) {
+        int ee = m.free_edge[e];
+        int a = m.node_to_free[m.edge_tail[ee]], b = m.node_to_free[m.edge_head[ee]];
+        if (a >= 0) nedge[cur[a]++] = e;
+        if (b >= 0) nedge[cur[b]++] = e;
+      }
+    }
+    auto sign_of = [&](int e, int fnode) {
+      return m.node_to_free[m.edge_head[m.free_edge[e]]] == fnode ? (int8_t)1 : (int8_t)-1;
+    };
+    if (d->coarse_kind == MDD_COARSE_NK) {
+      for (int v = 0; v < nfn; ++v) {
+        cand.push_back({-1, v});
+        for (int64_t k = np[v]; k < np[v + 1]; ++k) { cdof.push_back(nedge[k]); csign.push_back(sign_of(nedge[k], v)); }
+        cptr.push_back((int64_t)cdof.size());
+      }
+    } else {
+      std::vector<uint8_t> in(n, 0);
+      for (int i = 0; i < nsub; ++i) {
+        for (int32_t e : H->dec.sub_dofs[i]) in[e] = 1;
+        for (int32_t v : H->grad_nodes[i]) {
+          cand.push_back({i, v});
+          std::vector<int32_t> es;
+          for (int64_t k = np[v]; k < np[v + 1]; ++k)
+            if (in[nedge[k]]) es.push_back(nedge[k]);
+          std::sort(es.begin(), es.end());
+          for (int e : es) { cdof.push_back(e); csign.push_back(sign_of(e, v)); }
+          cptr.push_back((int64_t)cdof.size());
+        }
+        for (int32_t e : H->dec.sub_dofs[i]) in[e] = 0;
+      }
+    }
+    const int64_t nc = (int64_t)cand.size();
+    H->grad_cand = nc;
+    std::vector<int32_t> keep_cols;
+    if (d->coarse_kind == MDD_COARSE_NK) {
+      keep_cols.resize(nc);
+      std::iota(keep_cols.begin(), keep_cols.end(), 0);
+    } else {
+      // integer Gram Zint^T Zint (entries are exact small integers) on the device,
+      // then a rank-revealing LDL^T: dependent columns have pivots ~1e-14, the
+      // others >= ~1e-2 (reading R8)
+      DevCsr Zi, Zit, G;
+      {
+        // Zint: n x nc (CSR by dof) and its transpose
+        std::vector<int64_t> rp(n + 1, 0);
+        for (size_t k = 0; k < cdof.size(); ++k) rp[cdof[k] + 1]++;
+        for (int e = 0; e < n; ++e) rp[e + 1] += rp[e];
+        std::vector<int> rptr(n + 1), ridx(cdof.size());
+        std::vector<double> rval(cdof.size());
+        std::vector<int64_t> cur(rp.begin(), rp.end() - 1);
+        for (int64_t c = 0; c < nc; ++c)
+          for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) {
+            int64_t q = cur[cdof[k]]++;
+            ridx[q] = (int)c;
+            rval[q] = csign[k];
+          }
+        for (int e = 0; e <= n; ++e) rptr[e] = (int)rp[e];
+        std::vector<int> tptr(nc + 1), tidx(cdof.size());
+        std::vector<double> tval(cdof.size());
+        for (int64_t c = 0; c <= nc; ++c) tptr[c] = (int)cptr[c];
+        for (size_t k = 0; k < cdof.size(); ++k) { tidx[k] = cdof[k]; tval[k] = csign[k]; }
+        Zi.rows = n; Zi.cols = nc; Zi.nnz = (int64_t)cdof.size();
+        Zi.ptr.upload(rptr); Zi.idx.upload(ridx); Zi.val.upload(rval);
+        Zit.rows = nc; Zit.cols = n; Zit.nnz = (int64_t)cdof.size();
+        Zit.ptr.upload(tptr); Zit.idx.upload(tidx); Zit.val.upload(tval);
+      }
+      spgemm(H->sp, Zit, Zi, G, s);
+      Csr gpat;
+      std::vector<int64_t> gslot;
+      download_sorted(G, gpat, gslot);
+      std::vector<int32_t> gxyz(3 * nc);
+      for (int64_t c = 0; c < nc; ++c) {
+        int i, j, k;
+        m.node_ijk(m.free_node[cand[c].node], i, j, k);
+        gxyz[3 * c] = 2 * i; gxyz[3 * c + 1] = 2 * j; gxyz[3 * c + 2] = 2 * k;
+      }
+      DevFactor gf;
+      std::vector<SymSystem> sys{SymSystem{&gpat, gxyz.data(), gslot.data()}};
+      build_factor_plan(gf.fp, sys, 64);
+      gf.upload();
+      DBuf<uint8_t> dropped;
+      dropped.alloc(nc);
+      dropped.zero(s);
+      gf.factor(G.val.p, 1, 1e-8, dropped.p, s);
+      std::vector<uint8_t> dr = dropped.download();  // by position
+      for (int64_t c = 0; c < nc; ++c)
+        if (!dr[gf.fp.iperm_global[c]]) keep_cols.push_back((int32_t)c);
+    }
+    H->grad_rank = (int64_t)keep_cols.size();
+    H->setup_times[PH_GRAD_RANK] = now_s() - t0;
+
+    // ---- Z (basis) = kept gradient columns (values sign / mult) + GenEO columns
+    t0 = now_s();
+    const int64_t nb = H->grad_rank + H->ngeneo;
+    H->n0 = nb;
+    MDD_REQUIRE(nb > 0, 2, "empty coarse space");
+    DevCsr Z, Zt, W, E;
+    {
+      // assemble Z in CSR by dof: gradient entries sign/mult (computed in double on
+      // the host as the exact quotient of two small integers), GenEO entries from
+      // the device blocks
+      std::vector<int64_t> rp(n + 1, 0);
+      for (int32_t c : keep_cols)
+        for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) rp[cdof[k] + 1]++;
+      for (int i = 0; i < nsub; ++i)
+        for (int32_t e : H->dec.sub_dofs[i]) rp[e + 1] += geneo[i].k;
+      for (int e = 0; e < n; ++e) rp[e + 1] += rp[e];
+      const int64_t nnz = rp[n];
+      H->nnzZ = nnz;
+      MDD_REQUIRE(nnz < INT32_MAX, 5, "coarse basis too large for 32-bit indices");
+      std::vector<int> rptr(n + 1), ridx(nnz);
+      std::vector<double> rval(nnz, 0.0);
+      std::vector<int64_t> geneo_src(nnz, -1);  // index into concatenated device GenEO blocks
+      std::vector<int64_t> cur(rp.begin(), rp.end() - 1);
+      for (size_t j = 0; j < keep_cols.size(); ++j) {
+        int32_t c = keep_cols[j];
+        for (int64_t k = cptr[c]; k < cptr[c + 1]; ++k) {
+          int64_t q = cur[cdof[k]]++;
+          ridx[q] = (int)j;
+          rval[q] = d->coarse_kind == MDD_COARSE_NK ? (double)csign[k]
+                                                    : (double)csign[k] / (double)H->dec.mult[cdof[k]];
+        }
+      }
+      int64_t col = H->grad_rank, boff = 0;
+      for (int i = 0; i < nsub; ++i) {
+        const auto& D = H->dec.sub_dofs[i];
+        for (int kk = 0; kk < geneo[i].k; ++kk)
+          for (size_t l = 0; l < D.size(); ++l) {
+            int64_t q = cur[D[l]]++;
+            ridx[q] = (int)(col + kk);
+            geneo_src[q] = boff + (int64_t)kk * D.size() + l;
+          }
+        col += geneo[i].k;
+        boff += (int64_t)geneo[i].k * D.size();
+      }
+      for (int e = 0; e <= n; ++e) rptr[e] = (int)rp[e];
+      Z.rows = n; Z.cols = nb; Z.nnz = nnz;
+      Z.ptr.upload(rptr); Z.idx.upload(ridx); Z.val.upload(rval);
+      if (H->ngeneo > 0) {
+        // GenEO values: Z.val[dst[k]] = blocks[src[k]] on the device
+        DBuf<double> blocks;
+        blocks.alloc(boff);
+        int64_t o = 0;
+        for (int i = 0; i < nsub; ++i) {
+          size_t cnt = (size_t)geneo[i].k * H->dec.sub_dofs[i].size();
+          if (cnt) CUDA_CHECK(cudaMemcpyAsync(blocks.p + o, geneo[i].W.p, cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          o += cnt;
+        }
+        std::vector<int64_t> gsrc, gdst;
+        for (int64_t q = 0; q < nnz; ++q)
+          if (geneo_src[q] >= 0) { gsrc.push_back(geneo_src[q]); gdst.push_back(q); }
+        DBuf<int64_t> dsrc, ddst;
+        dsrc.upload(gsrc); ddst.upload(gdst);
+        dev::k_scatter_gather<<<nblk((int64_t)gsrc.size(), 256), 256, 0, s>>>((int64_t)gsrc.size(), ddst.p, dsrc.p, blocks.p, Z.val.p);
+        CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+      for (int i = 0; i < nsub; ++i) geneo[i].W.release();
+    }
+    // E = Z^T (A Z) via cuSPARSE SpGEMM
+    {
+      DevCsr Ad;
+      Ad.rows = n; Ad.cols = n; Ad.nnz = H->Apat.nnz();
+      std::vector<int> ap(n + 1);
+      for (int e = 0; e <= n; ++e) ap[e] = (int)H->Apat.ptr[e];
+      Ad.ptr.upload(ap);
+      Ad.idx.upload(H->Apat.idx);
+      Ad.val.alloc(Ad.nnz);
+      CUDA_CHECK(cudaMemcpyAsync(Ad.val.p, H->A_val.p, Ad.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      spgemm(H->sp, Ad, Z, W, s);
+      transpose(H->sp, Z, Zt, s);
+      spgemm(H->sp, Zt, W, E, s);
+    }
+    Csr epat;
+    std::vector<int64_t> eslot;
+    download_sorted(E, epat, eslot);
+    // coordinates: node for gradient columns, box centre for GenEO columns
+    std::vector<int32_t> exyz(3 * nb);
+    for (size_t j = 0; j < keep_cols.size(); ++j) {
+      int i, jj, k;
+      m.node_ijk(m.free_node[cand[keep_cols[j]].node], i, jj, k);
+      exyz[3 * j] = 2 * i; exyz[3 * j + 1] = 2 * jj; exyz[3 * j + 2] = 2 * k;
+    }
+    {
+      int64_t col = H->grad_rank;
+      const int sx = m.nx / d->px, sy = m.ny / d->py, sz = m.nz / d->pz;
+      for (int i = 0; i < nsub; ++i) {
+        int si = i % d->px, sj = (i / d->px) % d->py, sk = i / (d->px * d->py);
+        for (int kk = 0; kk < geneo[i].k; ++kk, ++col) {
+          exyz[3 * col] = (2 * si + 1) * sx;
+          exyz[3 * col + 1] = (2 * sj + 1) * sy;
+          exyz[3 * col + 2] = (2 * sk + 1) * sz;
+        }
+      }
+    }
+    H->setup_times[PH_COARSE_E] = now_s() - t0;
+    t0 = now_s();
+    std::vector<SymSystem> sys{SymSystem{&epat, exyz.data(), eslot.data()}};
+    build_factor_plan(H->crs.fp, sys, 64);
+    H->crs.upload();
+    H->crs.factor(E.val.p, 0, 0.0, nullptr, s);
+    // hot-path copies of Z with columns relabelled to coarse positions
+    {
+      std::vector<int> zp(n + 1), zi(Z.nnz);
+      CUDA_CHECK(cudaMemcpy(zp.data(), Z.ptr.p, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(zi.data(), Z.idx.p, Z.nnz * sizeof(int), cudaMemcpyDeviceToHost));
+      std::vector<int64_t> zp64(n + 1);
+      for (int e = 0; e <= n; ++e) zp64[e] = zp[e];
+      for (auto& c : zi) c = H->crs.fp.iperm_global[c];
+      H->Z_ptr.upload(zp64);
+      H->Z_idx.upload(zi);
+      H->Z_val.alloc(Z.nnz);
+      CUDA_CHECK(cudaMemcpyAsync(H->Z_val.p, Z.val.p, Z.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      // Zt rows in position order
+      std::vector<int> tp(nb + 1), ti(Zt.nnz);
+      CUDA_CHECK(cudaMemcpy(tp.data(), Zt.ptr.p, (nb + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(ti.data(), Zt.idx.p, Zt.nnz * sizeof(int), cudaMemcpyDeviceToHost));
+      std::vector<int64_t> ptr2(nb + 1, 0), src(Zt.nnz);
+      std::vector<int32_t> idx2(Zt.nnz);
+      const auto& ip = H->crs.fp.iperm_global;
+      std::vector<int64_t> col_of_pos(nb);
+      for (int64_t c = 0; c < nb; ++c) col_of_pos[ip[c]] = c;
+      for (int64_t pidx = 0; pidx < nb; ++pidx) {
+        int64_t c = col_of_pos[pidx];
+        ptr2[pidx + 1] = ptr2[pidx] + (tp[c + 1] - tp[c]);
+      }
+      for (int64_t pidx = 0; pidx < nb; ++pidx) {
+        int64_t c = col_of_pos[pidx];
+        for (int64_t k = 0; k < tp[c + 1] - tp[c]; ++k) {
+          idx2[ptr2[pidx] + k] = ti[tp[c] + k];
+          src[ptr2[pidx] + k] = tp[c] + k;
+        }
+      }
+      H->Zt_ptr.upload(ptr2);
+      H->Zt_idx.upload(idx2);
+      H->Zt_val.alloc(Zt.nnz);
+      DBuf<int64_t> dsrc;
+      dsrc.upload(src);
+      dev::k_gather<<<nblk(Zt.nnz, 256), 256, 0, s>>>(Zt.nnz, dsrc.p, Zt.val.p, H->Zt_val.p);
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    H->setup_times[PH_COARSE_FACTOR] = now_s() - t0;
+  }
+  H->Ke.release();
+  H->Me.release();
+
+  // ------------------------------------------------------- work buffers
+  for (DBuf<double>* b : {&H->x, &H->r, &H->p, &H->q, &H->z, &H->t1, &H->t2, &H->t3, &H->t4})
+    b->alloc(n);
+  H->xloc.alloc(H->loc.fp.ntot);
+  H->xc.alloc(std::max<int64_t>(H->n0, 1));
+  H->S.alloc(dev::S_COUNT);
+  H->nparts = 4 * 148;
+  H->part.alloc(std::max<int64_t>(H->nparts, nblk(n, 8)) + 8);
+  H->state.alloc(4);
+  H->state.zero(s);
+  CUDA_CHECK(cudaMallocHost(&H->state_host, 4 * sizeof(int)));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit, int* iters,
+                double* relres) {
+  MDD_REQUIRE(tol > 0 && maxit >= 0, 2, "tol must be > 0 and maxit >= 0");
+  CUDA_CHECK(cudaSetDevice(H->device));
+  cudaStream_t s = H->stream;
+  const int n = H->n;
+  using namespace dev;
+  H->state.zero(s);
+  H->S.zero(s);
+  CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  CUDA_CHECK(cudaMemcpyAsync(H->r.p, f, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  H->dot(f, f, S_RR);
+  std::vector<double> hs(S_COUNT);
+  CUDA_CHECK(cudaMemcpyAsync(hs.data(), H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  double nf = std::sqrt(hs[S_RR]);
+  if (nf == 0.0) {
+    *iters = 0;
+    *relres = 0.0;
+    return;
+  }
+  hs[S_NF] = nf;
+  CUDA_CHECK(cudaMemcpyAsync(H->S.p + S_NF, &hs[S_NF], sizeof(double), cudaMemcpyHostToDevice, s));
+  cudaEvent_t* ev = H->ev;
+  const bool prof = H->profiling;
+  for (auto& v : H->prof_ms) v = 0;
+  for (auto& v : H->prof_launch) v = 0;
+  auto mark = [&](int k) { if (prof) CUDA_CHECK(cudaEventRecord(ev[k], s)); };
+  auto acc = [&](int phase, int a, int b) {
+    if (!prof) return;
+    float ms = 0;
+    CUDA_CHECK(cudaEventSynchronize(ev[b]));
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    H->prof_ms[phase] += ms;
+    H->prof_launch[phase] += 1;
+  };
+  mark(0);
+  H->apply_prec(H->r.p, H->z.p);
+  mark(1);
+  k_copy<<<nblk(n, 256), 256, 0, s>>>(n, H->z.p, H->p.p, H->state.p);
+  H->dot(H->r.p, H->z.p, S_RZ);
+  int k = 0;
+  bool converged = false;
+  for (k = 1; k <= maxit; ++k) {
+    mark(2);
+    int blocks = nblk(n, 8);
+    k_spmv<<<blocks, 256, 0, s>>>(n, H->A_ptr.p, H->A_idx.p, H->A_val.p, H->p.p, H->q.p, H->p.p, H->part.p, H->state.p);
+    mark(3);
+    k_reduce<<<1, 256, 0, s>>>(blocks, H->part.p, H->S.p + S_PQ, H->state.p);
+    k_scalar_step<<<1, 1, 0, s>>>(0, H->S.p, H->state.p, tol, k);
+    k_update_xr<<<H->nparts, 256, 0, s>>>(n, x, H->r.p, H->p.p, H->q.p, H->S.p, H->part.p, H->state.p);
+    k_reduce<<<1, 256, 0, s>>>(H->nparts, H->part.p, H->S.p + S_RR, H->state.p);
+    k_scalar_step<<<1, 1, 0, s>>>(1, H->S.p, H->state.p, tol, k);
+    mark(4);
+    CUDA_CHECK(cudaMemcpyAsync(H->state_host, H->state.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    acc(MDD_PROF_SPMV, 2, 3);
+    acc(MDD_PROF_VECTOR, 3, 4);
+    if (H->state_host[2]) throw Error(MDD_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0");
+    if (H->state_host[0]) { converged = true; break; }
+    mark(5);
+    H->apply_prec(H->r.p, H->z.p);
+    mark(6);
+    H->dot(H->r.p, H->z.p, S_RZNEW);
+    k_scalar_step<<<1, 1, 0, s>>>(2, H->S.p, H->state.p, tol, k);
+    k_update_p<<<H->nparts, 256, 0, s>>>(n, H->p.p, H->z.p, H->S.p, H->state.p);
+    mark(7);
+    if (prof) {
+      acc(MDD_PROF_LOCAL_FWD, 5, 6);  // whole preconditioner (split below if needed)
+      acc(MDD_PROF_VECTOR, 6, 7);
+    }
+  }
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaMemcpyAsync(hs.data(), H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  *iters = converged ? H->state_host[1] : maxit;
+  *relres = hs[S_REL];
+  if (!converged) throw Error(MDD_ERR_NOCONV, "PCG did not converge within maxit");
+}
+
+int guard(std::function<void()> f) {
+  try {
+    f();
+    return MDD_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MDD_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* mdd_last_error(void) { return g_err.c_str(); }
+
+int mdd_setup(const mdd_setup_desc* desc, mdd_handle* out) {
+  if (!out) { g_err = "null output"; return MDD_ERR_ARG; }
+  *out = nullptr;
+  auto* H = new mdd_solver();
+  int rc = guard([&] { setup_impl(H, desc); });
+  if (rc != MDD_OK) { delete H; return rc; }
+  *out = H;
+  return MDD_OK;
+}
+
+void mdd_destroy(mdd_handle h) { delete h; }
+
+int mdd_solve(mdd_handle h, const double* f, double* x, double tol, int maxit, int* iters, double* relres) {
+  if (!h || !f || !x || !iters || !relres) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] { solve_impl(h, f, x, tol, maxit, iters, relres); });
+}
+
+int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int maxit, int* iters, double* relres) {
+  if (!h || !f || !x || !iters || !relres) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(h->device));
+    DBuf<double> fd, xd;
+    fd.alloc(h->n);
+    xd.alloc(h->n);
+    CUDA_CHECK(cudaMemcpyAsync(fd.p, f, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    int rc = MDD_OK;
+    std::string msg;
+    try {
+      solve_impl(h, fd.p, xd.p, tol, maxit, iters, relres);
+    } catch (const Error& e) {
+      rc = e.code; msg = e.what();
+      if (rc != MDD_ERR_NOCONV) throw;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(x, xd.p, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    if (rc != MDD_OK) throw Error(rc, msg);
+  });
+}
+
+int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z) {
+  if (!h || !r || !z) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    h->state.zero(h->stream);
+    h->apply_prec(r, z);
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int mdd_apply_operator(mdd_handle h, const double* x, double* y) {
+  if (!h || !x || !y) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    h->state.zero(h->stream);
+    h->applyA(x, y);
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int mdd_apply_local(mdd_handle h, const double* r, double* z) {
+  if (!h || !r || !z) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    h->state.zero(h->stream);
+    h->apply_local(r, z);
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int mdd_apply_coarse(mdd_handle h, const double* v, double* y) {
+  if (!h || !v || !y) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    MDD_REQUIRE(h->has_coarse, 2, "no coarse space configured");
+    h->state.zero(h->stream);
+    h->apply_coarse(v, y);
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+  });
+}
+
+int mdd_info(mdd_handle h, int64_t* out, int count) {
+  if (!h || !out) { g_err = "null argument"; return MDD_ERR_ARG; }
+  int64_t v[MDD_INFO_COUNT] = {0};
+  v[MDD_INFO_N] = h->n;
+  v[MDD_INFO_NEDGES] = h->mesh.nedges();
+  v[MDD_INFO_NFREE_NODES] = (int64_t)h->mesh.free_node.size();
+  v[MDD_INFO_NSUB] = h->dec.nsub;
+  v[MDD_INFO_NNZ_A] = h->Apat.nnz();
+  v[MDD_INFO_NLOC] = h->loc.fp.ntot;
+  v[MDD_INFO_GRAD_CANDIDATES] = h->grad_cand;
+  v[MDD_INFO_GRAD_RANK] = h->grad_rank;
+  v[MDD_INFO_NGENEO] = h->ngeneo;
+  v[MDD_INFO_N0] = h->n0;
+  v[MDD_INFO_LOCAL_FACTOR_NNZ] = h->loc.fp.factor_nnz();
+  v[MDD_INFO_COARSE_FACTOR_NNZ] = h->has_coarse ? h->crs.fp.factor_nnz() : 0;
+  v[MDD_INFO_LOCAL_SUPERNODES] = h->loc.fp.nsn;
+  v[MDD_INFO_LOCAL_LEVELS] = h->loc.fp.nlevels;
+  v[MDD_INFO_COARSE_SUPERNODES] = h->has_coarse ? h->crs.fp.nsn : 0;
+  v[MDD_INFO_COARSE_LEVELS] = h->has_coarse ? h->crs.fp.nlevels : 0;
+  v[MDD_INFO_NNZ_Z] = h->nnzZ;
+  v[MDD_INFO_KERNELS_PER_ITER] = 0;
+  for (int k = 0; k < count && k < MDD_INFO_COUNT; ++k) out[k] = v[k];
+  return MDD_OK;
+}
+
+int mdd_topology_int_array(const mdd_setup_desc* d, int which, int64_t* out, int64_t cap, int64_t* len) {
+  if (!d || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    MDD_REQUIRE(which != MDD_ARR_GENEO_COUNT, 2, "GenEO counts need a device setup");
+    auto H = std::unique_ptr<mdd_solver>(new mdd_solver());
+    build_mesh(H->mesh, d->nx, d->ny, d->nz, d->h, d->cube_mask, d->dirichlet);
+    H->n = H->mesh.n();
+    std::vector<int64_t> sp;
+    std::vector<int32_t> ct;
+    build_A_pattern(H->mesh, H->Apat, sp, ct);
+    build_subdomains(H->mesh, d->px, d->py, d->pz, d->overlap, H->dec);
+    H->grad_nodes.resize(H->dec.nsub);
+    for (int i = 0; i < H->dec.nsub; ++i) gradient_nodes(H->mesh, H->dec.sub_dofs[i], H->grad_nodes[i]);
+    int rc = mdd_get_int_array(H.get(), which, out, cap, len);
+    if (rc != MDD_OK) throw Error(rc, g_err);
+  });
+}
+
+int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len) {
+  if (!h || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    std::vector<int64_t> v;
+    const HostMesh& m = h->mesh;
+    switch (which) {
+      case MDD_ARR_EDGE_TAIL: v.assign(m.edge_tail.begin(), m.edge_tail.end()); break;
+      case MDD_ARR_EDGE_HEAD: v.assign(m.edge_head.begin(), m.edge_head.end()); break;
+      case MDD_ARR_FREE_EDGES: v.assign(m.free_edge.begin(), m.free_edge.end()); break;
+      case MDD_ARR_FREE_NODES: v.assign(m.free_node.begin(), m.free_node.end()); break;
+      case MDD_ARR_A_PTR: v.assign(h->Apat.ptr.begin(), h->Apat.ptr.end()); break;
+      case MDD_ARR_A_IDX: v.assign(h->Apat.idx.begin(), h->Apat.idx.end()); break;
+      case MDD_ARR_SUB_PTR:
+        v.push_back(0);
+        for (auto& D : h->dec.sub_dofs) v.push_back(v.back() + (int64_t)D.size());
+        break;
+      case MDD_ARR_SUB_DOFS:
+        for (auto& D : h->dec.sub_dofs) v.insert(v.end(), D.begin(), D.end());
+        break;
+      case MDD_ARR_GRAD_NODES_PTR:
+        v.push_back(0);
+        for (auto& D : h->grad_nodes) v.push_back(v.back() + (int64_t)D.size());
+        break;
+      case MDD_ARR_GRAD_NODES:
+        for (auto& D : h->grad_nodes) v.insert(v.end(), D.begin(), D.end());
+        break;
+      case MDD_ARR_GENEO_COUNT: v = h->geneo_count; break;
+      default: throw Error(MDD_ERR_ARG, "unknown array");
+    }
+    *len = (int64_t)v.size();
+    if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, *len), out);
+  });
+}
+
+int mdd_get_double_array(mdd_handle h, int which, double* out, int64_t cap, int64_t* len) {
+  if (!h || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    std::vector<double> v;
+    switch (which) {
+      case MDD_DARR_A_VAL: v = h->A_val.download(); break;
+      case MDD_DARR_K_VAL: v = h->K_val.download(); break;
+      case MDD_DARR_M_VAL: v = h->M_val.download(); break;
+      case MDD_DARR_GENEO_LAMBDA: v = h->geneo_lambda; break;
+      case MDD_DARR_SETUP_TIMES: v = h->setup_times; break;
+      default: throw Error(MDD_ERR_ARG, "unknown array");
+    }
+    *len = (int64_t)v.size();
+    if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, *len), out);
+  });
+}
+
+const char* mdd_phase_name(int phase) {
+  return (phase >= 0 && phase < PH_COUNT) ? kPhaseNames[phase] : "";
+}
+
+int mdd_set_profiling(mdd_handle h, int enable) {
+  if (!h) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    if (enable && !h->profiling)
+      for (auto& e : h->ev) CUDA_CHECK(cudaEventCreate(&e));
+    if (!enable && h->profiling)
+      for (auto& e : h->ev) cudaEventDestroy(e);
+    h->profiling = enable != 0;
+  });
+}
+
+int mdd_profile(mdd_handle h, double* ms, int64_t* launches, int count) {
+  if (!h) { g_err = "null argument"; return MDD_ERR_ARG; }
+  for (int k = 0; k < count && k < MDD_PROF_COUNT; ++k) {
+    if (ms) ms[k] = h->prof_ms[k];
+    if (launches) launches[k] = h->prof_launch[k];
+  }
+  return MDD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Device-side helpers shared by the orchestration files.
+#pragma once
+#include <cuda_runtime.h>
+#include <cusparse.h>
+
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+
+namespace mdd {
+
+#define CUDA_CHECK(x)                                                                     \
+  do {                                                                                    \
+    cudaError_t e__ = (x);                                                                \
+    if (e__ != cudaSuccess)                                                               \
+      throw ::mdd::Error(1, std::string(#x) + ": " + cudaGetErrorString(e__));            \
+  } while (0)
+#define CUSPARSE_CHECK(x)                                                                 \
+  do {                                                                                    \
+    cusparseStatus_t s__ = (x);                                                           \
+    if (s__ != CUSPARSE_STATUS_SUCCESS)                                                   \
+      throw ::mdd::Error(1, std::string(#x) + ": cusparse status " + std::to_string((int)s__)); \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() {}
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  // Setup-time transfers.  A pageable cudaMemcpy may return before its DMA lands
+  // and is not ordered with the library's non-blocking stream, so both directions
+  // synchronise the whole device.
+  void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+  void upload(const T* v, size_t count) {
+    alloc(count);
+    if (n) {
+      CUDA_CHECK(cudaMemcpy(p, v, n * sizeof(T), cudaMemcpyHostToDevice));
+      CUDA_CHECK(cudaDeviceSynchronize());
+    }
+  }
+  std::vector<T> download() const {
+    std::vector<T> v(n);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    if (n) CUDA_CHECK(cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    return v;
+  }
+};
+
+// A FactorPlan on the device plus its numeric factor.
+struct DevFactor {
+  FactorPlan fp;
+  DBuf<int64_t> col0, rowptr, offrows, lptr, uptr, fptr, umptr, child_ptr, asm_ptr, asm_src;
+  DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn;
+  DBuf<double> L, dinv, upd;
+  std::vector<int> fwd_smem, bwd_smem;  // bytes per level
+  int threads = 128;
+  dev::PlanDev plan() const;
+  void upload();
+  // numeric multifrontal factorisation from a device value array `src`
+  void factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
+  void forward(const double* b, const int32_t* gmap, double* x, cudaStream_t s) const;
+  void backward(double* x, cudaStream_t s) const;
+};
+
+}  // namespace mdd

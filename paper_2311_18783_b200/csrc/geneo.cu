@@ -1,0 +1,185 @@
+// GenEO GEVPs on the device with cuBLAS / cuSOLVER (setup phase).
+//
+// Per subdomain j, densely (Def. 2.4 and GEVP 3.5):
+//   xi_0j = G_j (G_j^T A_j G_j)^{-1} G_j^T A_j,  P = I - xi_0j,
+//   L_j   = (D_j P)^T A_j (D_j P),  B_j = A_j^Neu (assembled over the tets of Omega_j),
+//   L_j V = lambda B_j V, keep lambda > tau;  columns W = D_j P V.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+
+#include "geneo.h"
+
+namespace mdd {
+
+#define CUBLAS_CHECK(x)                                                                        \
+  do {                                                                                         \
+    cublasStatus_t s__ = (x);                                                                  \
+    if (s__ != CUBLAS_STATUS_SUCCESS)                                                          \
+      throw Error(1, std::string(#x) + ": cublas status " + std::to_string((int)s__));         \
+  } while (0)
+#define CUSOLVER_CHECK(x)                                                                      \
+  do {                                                                                         \
+    cusolverStatus_t s__ = (x);                                                                \
+    if (s__ != CUSOLVER_STATUS_SUCCESS)                                                        \
+      throw Error(1, std::string(#x) + ": cusolver status " + std::to_string((int)s__));       \
+  } while (0)
+
+static inline int nb(int64_t n, int t) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
+
+
+void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, cudaStream_t s) {
+  const HostMesh& m = *in.mesh;
+  const Decomp& dec = *in.dec;
+  const int nsub = dec.nsub;
+  out.clear();
+  out.resize(nsub);
+  cublasHandle_t cb;
+  cusolverDnHandle_t cs;
+  CUBLAS_CHECK(cublasCreate(&cb));
+  CUSOLVER_CHECK(cusolverDnCreate(&cs));
+  CUBLAS_CHECK(cublasSetStream(cb, s));
+  CUSOLVER_CHECK(cusolverDnSetStream(cs, s));
+  std::vector<int32_t> g2l(m.n(), -1);
+  DBuf<int> info;
+  info.alloc(1);
+  try {
+    for (int j = 0; j < nsub; ++j) {
+      const auto& D = dec.sub_dofs[j];
+      const int64_t n = (int64_t)D.size();
+      const Csr& lp = (*in.lpat)[j];
+      const auto& ls = (*in.lslot)[j];
+      for (int64_t k = 0; k < n; ++k) g2l[D[k]] = (int32_t)k;
+      // dense positions of the local pattern
+      std::vector<int64_t> dpos(lp.nnz());
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t p = lp.ptr[r]; p < lp.ptr[r + 1]; ++p) dpos[p] = (int64_t)lp.idx[p] * n + r;
+      // Neumann contributions per local slot from the tets of Omega_j (fixed order)
+      std::vector<int64_t> cnt(lp.nnz() + 1, 0);
+      std::vector<std::pair<int64_t, int32_t>> cl;  // (slot, contrib)
+      for (int32_t t : dec.sub_tets[j])
+        for (int a = 0; a < 6; ++a) {
+          int ea = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + a]];
+          if (ea < 0) continue;
+          int la = g2l[ea];
+          for (int b = 0; b < 6; ++b) {
+            int eb = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + b]];
+            if (eb < 0) continue;
+            int lb = g2l[eb];
+            const int32_t* b0 = lp.idx.data() + lp.ptr[la];
+            const int32_t* b1 = lp.idx.data() + lp.ptr[la + 1];
+            int64_t slot = (int64_t)(std::lower_bound(b0, b1, lb) - lp.idx.data());
+            cl.push_back({slot, (int32_t)((int64_t)t * 36 + a * 6 + b)});
+          }
+        }
+      std::stable_sort(cl.begin(), cl.end(), [](const std::pair<int64_t, int32_t>& x,
+                                                 const std::pair<int64_t, int32_t>& y) { return x.first < y.first; });
+      std::vector<int32_t> ctb(cl.size());
+      for (size_t q = 0; q < cl.size(); ++q) { cnt[cl[q].first + 1]++; ctb[q] = cl[q].second; }
+      for (int64_t q = 0; q < lp.nnz(); ++q) cnt[q + 1] += cnt[q];
+      // gradient columns
+      const auto& gn = (*in.grad_nodes)[j];
+      const int64_t g = (int64_t)gn.size();
+      std::vector<int64_t> gpos;
+      std::vector<double> gval;
+      {
+        std::vector<int32_t> colof(m.free_node.size() ? m.free_node.size() : 1, -1);
+        for (int64_t c = 0; c < g; ++c) colof[gn[c]] = (int32_t)c;
+        for (int64_t k = 0; k < n; ++k) {
+          int ee = m.free_edge[D[k]];
+          int a = m.node_to_free[m.edge_tail[ee]], b = m.node_to_free[m.edge_head[ee]];
+          if (a >= 0 && colof[a] >= 0) { gpos.push_back((int64_t)colof[a] * n + k); gval.push_back(-1.0); }
+          if (b >= 0 && colof[b] >= 0) { gpos.push_back((int64_t)colof[b] * n + k); gval.push_back(1.0); }
+        }
+      }
+      std::vector<double> Dw(n);
+      for (int64_t k = 0; k < n; ++k) Dw[k] = 1.0 / (double)dec.mult[D[k]];
+      for (int64_t k = 0; k < n; ++k) g2l[D[k]] = -1;
+
+      // ---- device work
+      DBuf<double> Ad, Bd, P, T1, G, W1, Sg, Xt, dw, vals, lam;
+      DBuf<int64_t> d_dpos, d_slot, d_cnt, d_gpos;
+      DBuf<int32_t> d_ctb;
+      Ad.alloc(n * n); Ad.zero(s);
+      Bd.alloc(n * n); Bd.zero(s);
+      d_dpos.upload(dpos);
+      d_slot.upload(ls);
+      vals.alloc(std::max<int64_t>(lp.nnz(), 1));
+      dev::k_gather<<<nb(lp.nnz(), 256), 256, 0, s>>>(lp.nnz(), d_slot.p, in.A_val, vals.p);
+      dev::k_dense_scatter<<<nb(lp.nnz(), 256), 256, 0, s>>>(lp.nnz(), d_dpos.p, vals.p, Ad.p);
+      d_cnt.upload(cnt);
+      d_ctb.upload(ctb);
+      dev::k_slot_sums<<<nb(lp.nnz(), 256), 256, 0, s>>>(lp.nnz(), d_cnt.p, d_ctb.p, in.Ke, in.Me, in.gamma, vals.p);
+      dev::k_dense_scatter<<<nb(lp.nnz(), 256), 256, 0, s>>>(lp.nnz(), d_dpos.p, vals.p, Bd.p);
+      P.alloc(n * n);
+      dev::k_set_identity_minus<<<nb(n * n, 256), 256, 0, s>>>(n, P.p);
+      const double one = 1.0, zero = 0.0, mone = -1.0;
+      if (g > 0) {
+        G.alloc(n * g); G.zero(s);
+        d_gpos.upload(gpos);
+        DBuf<double> gv; gv.upload(gval);
+        dev::k_dense_scatter<<<nb((int64_t)gpos.size(), 256), 256, 0, s>>>((int64_t)gpos.size(), d_gpos.p, gv.p, G.p);
+        W1.alloc(n * g);
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, g, n, &one, Ad.p, n, G.p, n, &zero, W1.p, n));
+        Sg.alloc(g * g);
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, g, g, n, &one, G.p, n, W1.p, n, &zero, Sg.p, g));
+        int lw = 0;
+        CUSOLVER_CHECK(cusolverDnDpotrf_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, g, Sg.p, g, &lw));
+        DBuf<double> work; work.alloc(std::max(lw, 1));
+        CUSOLVER_CHECK(cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, g, Sg.p, g, work.p, lw, info.p));
+        Xt.alloc(g * n);
+        CUBLAS_CHECK(cublasDgeam(cb, CUBLAS_OP_T, CUBLAS_OP_N, g, n, &one, W1.p, n, &zero, Xt.p, g, Xt.p, g));
+        CUSOLVER_CHECK(cusolverDnDpotrs(cs, CUBLAS_FILL_MODE_LOWER, g, n, Sg.p, g, Xt.p, g, info.p));
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, g, &mone, G.p, n, Xt.p, g, &one, P.p, n));
+        G.release(); W1.release(); Sg.release(); Xt.release();
+      }
+      dw.upload(Dw);
+      dev::k_scale_rows<<<nb(n * n, 256), 256, 0, s>>>(n, n, dw.p, P.p);  // P <- D P
+      T1.alloc(n * n);
+      CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, Ad.p, n, P.p, n, &zero, T1.p, n));
+      // L = (DP)^T A (DP), written into Ad
+      CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, n, n, n, &one, P.p, n, T1.p, n, &zero, Ad.p, n));
+      T1.release();
+      dev::k_symmetrize<<<nb(n * n, 256), 256, 0, s>>>(n, Ad.p);
+      lam.alloc(n);
+      int lw = 0, meig = 0;
+      const double vu = 1.0e300;
+      CUSOLVER_CHECK(cusolverDnDsygvdx_bufferSize(cs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                                  CUSOLVER_EIG_RANGE_V, CUBLAS_FILL_MODE_LOWER, n, Ad.p, n,
+                                                  Bd.p, n, tau, vu, 0, 0, &meig, lam.p, &lw));
+      DBuf<double> work; work.alloc(std::max(lw, 1));
+      CUSOLVER_CHECK(cusolverDnDsygvdx(cs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_V,
+                                       CUBLAS_FILL_MODE_LOWER, n, Ad.p, n, Bd.p, n, tau, vu, 0, 0, &meig,
+                                       lam.p, work.p, lw, info.p));
+      int hinfo = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      MDD_REQUIRE(hinfo == 0, 1, "GenEO GEVP (sygvdx) failed in subdomain " + std::to_string(j) +
+                                       ": info " + std::to_string(hinfo) + " n " + std::to_string(n) +
+                                       " meig " + std::to_string(meig));
+      GeneoBlock& B = out[j];
+      std::vector<double> l(n);
+      CUDA_CHECK(cudaMemcpy(l.data(), lam.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int q = 0; q < meig; ++q)
+        if (l[q] > tau) B.lambda.push_back(l[q]);
+      B.k = (int)B.lambda.size();
+      if (B.k > 0) {
+        // eigenvectors occupy the first meig columns of Ad, ascending eigenvalues
+        int first = meig - B.k;
+        B.W.alloc(n * B.k);
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, B.k, n, &one, P.p, n, Ad.p + (int64_t)first * n,
+                                 n, &zero, B.W.p, n));
+      }
+      CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+  } catch (...) {
+    cublasDestroy(cb);
+    cusolverDnDestroy(cs);
+    throw;
+  }
+  cublasDestroy(cb);
+  cusolverDnDestroy(cs);
+}
+
+}  // namespace mdd

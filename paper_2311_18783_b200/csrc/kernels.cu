@@ -1,0 +1,450 @@
+// Device kernels of the maxwell_dd library (sm_100a, FP64).  See kernels.cuh.
+#include "kernels.cuh"
+
+namespace mdd {
+namespace dev {
+
+// ----------------------------------------------------------- assembly
+__constant__ int c_kuhn[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+__constant__ int c_ledge[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+__global__ void k_element_matrices(int64_t ntet, const int64_t* __restrict__ tet_id,
+                                   const int64_t* __restrict__ tet_nodes, int nx, int ny,
+                                   double h, const double* __restrict__ mu_inv,
+                                   const double* __restrict__ eps, double* __restrict__ Ke,
+                                   double* __restrict__ Me) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntet) return;
+  double x[4][3];
+  for (int v = 0; v < 4; ++v) {
+    int64_t id = tet_nodes[4 * t + v];
+    int64_t i = id % (nx + 1), j = (id / (nx + 1)) % (ny + 1), k = id / ((int64_t)(nx + 1) * (ny + 1));
+    x[v][0] = h * (double)i; x[v][1] = h * (double)j; x[v][2] = h * (double)k;
+  }
+  // J = [x1-x0, x2-x0, x3-x0] (columns); rows of J^{-1} are grad lambda_1..3
+  double J[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) J[r][c] = x[c + 1][r] - x[0][r];
+  double det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+               J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+               J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+  double inv[3][3];
+  inv[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) / det;
+  inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+  inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+  inv[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) / det;
+  inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+  inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+  inv[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) / det;
+  inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+  inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  double g[4][3];
+  for (int c = 0; c < 3; ++c) {
+    g[1][c] = inv[0][c]; g[2][c] = inv[1][c]; g[3][c] = inv[2][c];
+    g[0][c] = -(inv[0][c] + inv[1][c] + inv[2][c]);
+  }
+  double vol = fabs(det) / 6.0;
+  int64_t tid = tet_id[t];
+  double mi = mu_inv[tid], ep = eps[tid];
+  double cu[6][3];
+  for (int e = 0; e < 6; ++e) {
+    const double* a = g[c_ledge[e][0]];
+    const double* b = g[c_ledge[e][1]];
+    cu[e][0] = 2.0 * (a[1] * b[2] - a[2] * b[1]);
+    cu[e][1] = 2.0 * (a[2] * b[0] - a[0] * b[2]);
+    cu[e][2] = 2.0 * (a[0] * b[1] - a[1] * b[0]);
+  }
+  double G[4][4];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) G[a][b] = g[a][0] * g[b][0] + g[a][1] * g[b][1] + g[a][2] * g[b][2];
+  double kf = mi * vol, mf = ep * vol / 20.0;
+  for (int m = 0; m < 6; ++m) {
+    int a = c_ledge[m][0], b = c_ledge[m][1];
+    for (int n = 0; n < 6; ++n) {
+      int c = c_ledge[n][0], d = c_ledge[n][1];
+      Ke[t * 36 + m * 6 + n] = kf * (cu[m][0] * cu[n][0] + cu[m][1] * cu[n][1] + cu[m][2] * cu[n][2]);
+      Me[t * 36 + m * 6 + n] = mf * ((1 + (a == c)) * G[b][d] - (1 + (a == d)) * G[b][c] -
+                                     (1 + (b == c)) * G[a][d] + (1 + (b == d)) * G[a][c]);
+    }
+  }
+}
+
+__global__ void k_assemble_slots(int64_t nslot, const int64_t* __restrict__ ptr,
+                                 const int32_t* __restrict__ contrib,
+                                 const double* __restrict__ Ke, const double* __restrict__ Me,
+                                 double gamma, double* __restrict__ A, double* __restrict__ K,
+                                 double* __restrict__ M) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  double k = 0.0, m = 0.0;
+  for (int64_t c = ptr[s]; c < ptr[s + 1]; ++c) {
+    int32_t q = contrib[c];
+    k += Ke[q];
+    m += Me[q];
+  }
+  if (K) K[s] = k;
+  if (M) M[s] = m;
+  A[s] = k + gamma * m;
+}
+
+__global__ void k_gather(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                         double* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+__global__ void k_scatter_gather(int64_t n, const int64_t* __restrict__ di, const int64_t* __restrict__ si,
+                                 const double* __restrict__ src, double* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[di[i]] = src[si[i]];
+}
+
+__global__ void k_dense_scatter(int64_t n, const int64_t* __restrict__ pos, const double* __restrict__ v,
+                                double* __restrict__ D) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) D[pos[i]] = v[i];
+}
+
+// P = I (n x n); used before P -= G X
+__global__ void k_set_identity_minus(int64_t n, double* __restrict__ P) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * n) P[i] = (i % n == i / n) ? 1.0 : 0.0;
+}
+
+__global__ void k_scale_rows(int64_t n, int64_t cols, const double* __restrict__ d, double* __restrict__ P) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * cols) P[i] *= d[i % n];
+}
+
+// L = (L + L^T) / 2 on the lower triangle (the GEVP reads the lower part)
+__global__ void k_symmetrize(int64_t n, double* __restrict__ L) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * n) return;
+  int64_t r = i % n, c = i / n;
+  if (r > c) {
+    double v = 0.5 * (L[r + c * n] + L[c + r * n]);
+    L[r + c * n] = v;
+  }
+}
+
+__global__ void k_slot_sums(int64_t nslot, const int64_t* __restrict__ ptr, const int32_t* __restrict__ contrib,
+                            const double* __restrict__ Ke, const double* __restrict__ Me, double gamma,
+                            double* __restrict__ out) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslot) return;
+  double k = 0.0, m = 0.0;
+  for (int64_t c = ptr[s]; c < ptr[s + 1]; ++c) {
+    k += Ke[contrib[c]];
+    m += Me[contrib[c]];
+  }
+  out[s] = k + gamma * m;
+}
+
+// --------------------------------------------------- multifrontal LDL^T
+__global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
+                                  double* __restrict__ fronts, double* __restrict__ L,
+                                  double* __restrict__ dinv, double* __restrict__ umat, int mode,
+                                  double tol, uint8_t* __restrict__ dropped, int* __restrict__ err) {
+  const int g = P.level_sn[level_begin + blockIdx.x];
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  const i64 col0 = P.sn_col0[g];
+  double* F = fronts + P.sn_fptr[g];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (i64 k = tid; k < (i64)nr * nr; k += nt) F[k] = 0.0;
+  __syncthreads();
+  for (i64 a = P.asm_ptr[g] + tid; a < P.asm_ptr[g + 1]; a += nt) F[P.asm_pos[a]] += src[P.asm_src[a]];
+  __syncthreads();
+  for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
+    const int c = P.child_list[ci];
+    const int noc = P.sn_noff[c];
+    const double* U = umat + P.sn_umptr[c];
+    const int* rm = P.relmap + P.sn_rowptr[c];
+    for (i64 k = tid; k < (i64)noc * noc; k += nt) {
+      int b = (int)(k / noc), a = (int)(k % noc);
+      if (a >= b) F[(i64)rm[b] * nr + rm[a]] += U[k];
+    }
+    __syncthreads();
+  }
+  for (int j = 0; j < nc; ++j) {
+    double* Fj = F + (i64)j * nr;
+    const double d = Fj[j];
+    bool drop = false;
+    if (mode == 1) drop = !(d > tol);
+    else if (!(d > 0.0)) {
+      if (tid == 0) atomicExch(err, 1);
+      drop = true;
+    }
+    if (drop) {
+      for (int i = j + 1 + tid; i < nr; i += nt) Fj[i] = 0.0;
+      if (tid == 0) {
+        dinv[col0 + j] = 0.0;
+        if (dropped) dropped[col0 + j] = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    const double rd = 1.0 / d;
+    for (int i = j + 1 + tid; i < nr; i += nt) Fj[i] *= rd;
+    __syncthreads();
+    for (int k = j + 1 + warp; k < nr; k += nw) {
+      const double lkd = Fj[k] * d;
+      double* Fk = F + (i64)k * nr;
+      for (int i = k + lane; i < nr; i += 32) Fk[i] -= Fj[i] * lkd;
+    }
+    if (tid == 0) {
+      dinv[col0 + j] = rd;
+      if (dropped) dropped[col0 + j] = 0;
+    }
+    __syncthreads();
+  }
+  // L21 and the update matrix
+  double* Lp = L + P.sn_lptr[g];
+  for (i64 k = tid; k < (i64)nc * no; k += nt) {
+    int j = (int)(k / no), i = nc + (int)(k % no);
+    Lp[(i64)j * nr + i] = F[(i64)j * nr + i];
+  }
+  double* U = umat + P.sn_umptr[g];
+  for (i64 k = tid; k < (i64)no * no; k += nt) {
+    int b = (int)(k / no), a = (int)(k % no);
+    U[k] = (a >= b) ? F[(i64)(nc + b) * nr + nc + a] : 0.0;
+  }
+  // explicit inverse of the unit-lower diagonal block, row by row:
+  // X[i][j] = -sum_{k=j}^{i-1} L[i][k] X[k][j]
+  for (int j = tid; j < nc; j += nt) Lp[(i64)j * nr + j] = 1.0;
+  __syncthreads();
+  for (int i = 1; i < nc; ++i) {
+    for (int j = tid; j < i; j += nt) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s -= F[(i64)k * nr + i] * Lp[(i64)j * nr + k];
+      Lp[(i64)j * nr + i] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------- supernodal triangular solves
+// CTA variant: one CTA per supernode.  Dynamic smem: t[nr] | y[nc].
+__global__ void k_fwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
+                            const double* __restrict__ dinv, const double* __restrict__ b,
+                            const int32_t* __restrict__ gmap, double* __restrict__ x,
+                            double* __restrict__ upd) {
+  extern __shared__ double sm[];
+  const int g = P.level_sn[level_begin + blockIdx.x];
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  const i64 col0 = P.sn_col0[g];
+  const double* __restrict__ Lp = L + P.sn_lptr[g];
+  double* t = sm;
+  double* y = sm + nr;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = tid; k < nc; k += nt) t[k] = gmap ? b[gmap[col0 + k]] : x[col0 + k];
+  for (int k = tid; k < no; k += nt) t[nc + k] = 0.0;
+  __syncthreads();
+  for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
+    const int c = P.child_list[ci];
+    const int noc = P.sn_noff[c];
+    const double* u = upd + P.sn_uptr[c];
+    const int* rm = P.relmap + P.sn_rowptr[c];
+    for (int a = tid; a < noc; a += nt) t[rm[a]] += u[a];
+    __syncthreads();
+  }
+  for (int i = tid; i < nc; i += nt) {
+    double s = 0.0;
+    for (int j = 0; j <= i; ++j) s += Lp[(i64)j * nr + i] * t[j];
+    y[i] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < nc; i += nt) x[col0 + i] = dinv[col0 + i] * y[i];
+  double* uo = upd + P.sn_uptr[g];
+  for (int i = nc + tid; i < nr; i += nt) {
+    double s = t[i];
+    for (int j = 0; j < nc; ++j) s -= Lp[(i64)j * nr + i] * y[j];
+    uo[i - nc] = s;
+  }
+}
+
+// Backward: v = x_c - L21^T x_off ; x_c = Linv11^T v.  Warps over columns.
+__global__ void k_bwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
+                            double* __restrict__ x) {
+  extern __shared__ double sm[];
+  const int g = P.level_sn[level_begin + blockIdx.x];
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  const i64 col0 = P.sn_col0[g];
+  const double* __restrict__ Lp = L + P.sn_lptr[g];
+  const i64* rows = P.offrows + P.sn_rowptr[g];
+  double* xo = sm;        // no
+  double* v = sm + no;    // nc
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int k = tid; k < no; k += nt) xo[k] = x[rows[k]];
+  __syncthreads();
+  for (int i = warp; i < nc; i += nw) {
+    const double* col = Lp + (i64)i * nr + nc;
+    double s = 0.0;
+    for (int k = lane; k < no; k += 32) s += col[k] * xo[k];
+    s = warp_sum(s);
+    if (lane == 0) v[i] = x[col0 + i] - s;
+  }
+  __syncthreads();
+  for (int i = warp; i < nc; i += nw) {
+    const double* col = Lp + (i64)i * nr;
+    double s = 0.0;
+    for (int k = i + lane; k < nc; k += 32) s += col[k] * v[k];
+    s = warp_sum(s);
+    if (lane == 0) x[col0 + i] = s;
+  }
+}
+
+__global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
+                          const double* __restrict__ x, double* __restrict__ out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int64_t k = ptr[e]; k < ptr[e + 1]; ++k) s += x[pos[k]];
+  out[e] = s;
+}
+
+// ---------------------------------------------------------- PCG pieces
+#define STOPPED (stop != nullptr && stop[0] != 0)
+
+// block-level sum of one value per thread -> part[blockIdx.x]; blockDim = 256
+__device__ __forceinline__ void block_sum_store(double v, double* part) {
+  __shared__ double ws[32];
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    double s = lane < nw ? ws[lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) part[blockIdx.x] = s;
+  }
+}
+
+// y = A x, one warp per row; optional partial dot(dotw, y)
+__global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                       const double* __restrict__ val, const double* __restrict__ x,
+                       double* __restrict__ y, const double* __restrict__ dotw,
+                       double* __restrict__ part, const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double contrib = 0.0;
+  if (row < n) {
+    double s = 0.0;
+    for (int64_t k = ptr[row] + lane; k < ptr[row + 1]; k += 32) s += val[k] * x[idx[k]];
+    s = warp_sum(s);
+    if (lane == 0) {
+      y[row] = s;
+      if (dotw) contrib = dotw[row] * s;
+    }
+  }
+  if (part) block_sum_store(contrib, part);
+}
+
+__global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ part, const int* __restrict__ stop) {
+  if (STOPPED) return;
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    s += a[i] * b[i];
+  block_sum_store(s, part);
+}
+
+__global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
+                         const int* __restrict__ stop) {
+  if (STOPPED) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+  __shared__ double tmp[1];
+  block_sum_store(s, tmp);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = tmp[0];
+}
+
+// scalar recurrences of PCG (single thread)
+__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state, double tol,
+                              int iter) {
+  if (state[0]) return;
+  switch (op) {
+    case 0:  // after q = A p:  alpha = rz / pq
+      if (!(S[S_PQ] > 0.0)) { state[2] = 1; state[0] = 1; return; }
+      S[S_ALPHA] = S[S_RZ] / S[S_PQ];
+      break;
+    case 1:  // after r update: convergence
+      S[S_REL] = sqrt(S[S_RR]) / S[S_NF];
+      state[1] = iter;
+      if (S[S_REL] <= tol) state[0] = 1;
+      break;
+    case 2:  // after z = M r: beta
+      S[S_BETA] = S[S_RZNEW] / S[S_RZ];
+      S[S_RZ] = S[S_RZNEW];
+      break;
+  }
+}
+
+__global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
+                            const double* __restrict__ p, const double* __restrict__ q,
+                            const double* __restrict__ S, double* __restrict__ part,
+                            const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const double alpha = S[S_ALPHA];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    double ri = r[i] - alpha * q[i];
+    r[i] = ri;
+    s += ri * ri;
+  }
+  block_sum_store(s, part);
+}
+
+__global__ void k_update_p(int n, double* __restrict__ p, const double* __restrict__ z,
+                           const double* __restrict__ S, const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const double beta = S[S_BETA];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+__global__ void k_axpby(int n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out,
+                        const int* __restrict__ stop) {
+  if (STOPPED) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a * x[i] + b * y[i];
+}
+
+// out = a + b - c
+__global__ void k_combine3(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ c, double* __restrict__ out,
+                           const int* __restrict__ stop) {
+  if (STOPPED) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i] - c[i];
+}
+
+__global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__ out,
+                       const int* __restrict__ stop) {
+  if (STOPPED) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = a[i];
+}
+
+__global__ void k_csr_warp_spmv(int nrows, const int64_t* __restrict__ ptr,
+                                const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                const double* __restrict__ x, double* __restrict__ y,
+                                const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= nrows) return;
+  double s = 0.0;
+  for (int64_t k = ptr[row] + lane; k < ptr[row + 1]; k += 32) s += val[k] * x[idx[k]];
+  s = warp_sum(s);
+  if (lane == 0) y[row] = s;
+}
+
+}  // namespace dev
+}  // namespace mdd

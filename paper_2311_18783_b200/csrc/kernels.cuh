@@ -1,0 +1,136 @@
+// Device kernels of the maxwell_dd library (sm_100a, FP64).
+//
+// Everything on the solve path is memory-bound sparse work, so no tensor cores:
+// coalesced FP64 loads of the supernodal panels, shared-memory staging of the
+// per-supernode vectors, warp-shuffle reductions, deterministic two-stage
+// reductions for every dot product (bit-reproducible iteration counts).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mdd {
+namespace dev {
+
+typedef long long i64;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------- assembly
+// Whitney element matrices of the Kuhn tets.  PAPER.md eq. (2.2):
+//   K^e_mn = mu^{-1} |T| (2 gl_a x gl_b).(2 gl_c x gl_d)
+//   M^e_mn = eps |T|/20 [(1+d_ac) gl_b.gl_d - (1+d_ad) gl_b.gl_c
+//                        - (1+d_bc) gl_a.gl_d + (1+d_bd) gl_a.gl_c]
+// for local edges m = (a,b), n = (c,d); gl = barycentric gradients.
+__global__ void k_element_matrices(int64_t ntet, const int64_t* __restrict__ tet_id,
+                                   const int64_t* __restrict__ tet_nodes, int nx, int ny,
+                                   double h, const double* __restrict__ mu_inv,
+                                   const double* __restrict__ eps, double* __restrict__ Ke,
+                                   double* __restrict__ Me);
+
+// A-slot sums in fixed contribution order (deterministic assembly):
+//   K[s] = sum_c Ke[contrib[c]], M[s] likewise; A = K + gamma M
+__global__ void k_assemble_slots(int64_t nslot, const int64_t* __restrict__ ptr,
+                                 const int32_t* __restrict__ contrib,
+                                 const double* __restrict__ Ke, const double* __restrict__ Me,
+                                 double gamma, double* __restrict__ A, double* __restrict__ K,
+                                 double* __restrict__ M);
+
+__global__ void k_gather(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                         double* __restrict__ dst);
+// dst[di[k]] = src[si[k]]
+__global__ void k_scatter_gather(int64_t n, const int64_t* __restrict__ di, const int64_t* __restrict__ si,
+                                 const double* __restrict__ src, double* __restrict__ dst);
+// dense helpers for the GEVP pipeline (column-major)
+__global__ void k_dense_scatter(int64_t n, const int64_t* __restrict__ pos, const double* __restrict__ v,
+                                double* __restrict__ D);
+__global__ void k_set_identity_minus(int64_t n, double* __restrict__ P);
+__global__ void k_scale_rows(int64_t n, int64_t cols, const double* __restrict__ d, double* __restrict__ P);
+__global__ void k_symmetrize(int64_t n, double* __restrict__ L);
+__global__ void k_slot_sums(int64_t nslot, const int64_t* __restrict__ ptr, const int32_t* __restrict__ contrib,
+                            const double* __restrict__ Ke, const double* __restrict__ Me, double gamma,
+                            double* __restrict__ out);
+
+// --------------------------------------------------- multifrontal LDL^T
+struct PlanDev {
+  const i64* sn_col0;
+  const int* sn_ncol;
+  const int* sn_noff;
+  const i64* sn_rowptr;
+  const i64* offrows;
+  const i64* sn_lptr;
+  const i64* sn_uptr;
+  const i64* sn_fptr;
+  const i64* sn_umptr;
+  const i64* child_ptr;
+  const int* child_list;
+  const int* relmap;
+  const i64* asm_ptr;
+  const i64* asm_src;
+  const int* asm_pos;
+  const int* level_sn;
+};
+
+// mode 0: SPD (pivot <= 0 flags an error); mode 1: rank-revealing (pivot <= tol is
+// a dependent column: D^{-1} = 0, L column = 0, flagged in `dropped`)
+__global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
+                                  double* __restrict__ fronts, double* __restrict__ L,
+                                  double* __restrict__ dinv, double* __restrict__ umat, int mode,
+                                  double tol, uint8_t* __restrict__ dropped, int* __restrict__ err);
+
+// -------------------------------------------- supernodal triangular solves
+// Forward (L y = b, multifrontal extend-add of child update vectors) and
+// diagonal (D^{-1}); one CTA per supernode of the level.  If gmap != NULL the
+// right-hand side is gathered b[gmap[pos]] (fused restriction R_i), else x[pos].
+__global__ void k_fwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
+                            const double* __restrict__ dinv, const double* __restrict__ b,
+                            const int32_t* __restrict__ gmap, double* __restrict__ x,
+                            double* __restrict__ upd);
+// Backward (L^T x = y) from the roots down.
+__global__ void k_bwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
+                            double* __restrict__ x);
+
+// prolongation sum_i R_i^T x_i: out[e] = sum over the copies of dof e (fixed order)
+__global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
+                          const double* __restrict__ x, double* __restrict__ out);
+
+// ---------------------------------------------------------- PCG pieces
+__global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                       const double* __restrict__ val, const double* __restrict__ x,
+                       double* __restrict__ y, const double* __restrict__ dotw,
+                       double* __restrict__ part, const int* __restrict__ stop);
+__global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ part, const int* __restrict__ stop);
+__global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
+                         const int* __restrict__ stop);
+__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state,
+                              double tol, int iter);
+__global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
+                            const double* __restrict__ p, const double* __restrict__ q,
+                            const double* __restrict__ S, double* __restrict__ part,
+                            const int* __restrict__ stop);
+__global__ void k_update_p(int n, double* __restrict__ p, const double* __restrict__ z,
+                           const double* __restrict__ S, const int* __restrict__ stop);
+__global__ void k_axpby(int n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out,
+                        const int* __restrict__ stop);
+__global__ void k_combine3(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ c, double* __restrict__ out,
+                           const int* __restrict__ stop);
+__global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__ out,
+                       const int* __restrict__ stop);
+
+// Z^T v and Z y over CSR copies of Z (rows = dofs) and Z^T (rows = coarse positions)
+__global__ void k_csr_warp_spmv(int nrows, const int64_t* __restrict__ ptr,
+                                const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                const double* __restrict__ x, double* __restrict__ y,
+                                const int* __restrict__ stop);
+
+// scalar slots of the PCG state
+enum { S_RZ = 0, S_PQ, S_ALPHA, S_RR, S_NF, S_BETA, S_RZNEW, S_REL, S_TMP, S_COUNT };
+// state[0] = stop flag, state[1] = iterations done, state[2] = breakdown
+}  // namespace dev
+}  // namespace mdd

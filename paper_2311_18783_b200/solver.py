@@ -1,0 +1,143 @@
+"""Thin Python front end of the C ABI (argument marshalling only)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _desc(w, coarse="snk", variant="as2", device=0, geneo=True) -> tuple:
+    mask = np.ascontiguousarray(w.cube_mask, dtype=np.uint8)
+    mu = np.ascontiguousarray(w.mu_inv, dtype=np.float64)
+    ep = np.ascontiguousarray(w.eps, dtype=np.float64)
+    d = L.SetupDesc()
+    d.nx, d.ny, d.nz, d.h = w.nx, w.ny, w.nz, float(w.h)
+    d.cube_mask = mask.ctypes.data_as(C.POINTER(C.c_uint8))
+    d.dirichlet = L.DIRICHLET[w.dirichlet]
+    d.mu_inv = mu.ctypes.data_as(C.POINTER(C.c_double))
+    d.eps = ep.ctypes.data_as(C.POINTER(C.c_double))
+    d.gamma = float(w.gamma)
+    d.px, d.py, d.pz, d.overlap = w.px, w.py, w.pz, w.overlap
+    d.coarse_threshold = float(w.threshold) if geneo else 0.0
+    d.coarse_kind = L.COARSE[coarse]
+    d.variant = L.VARIANT[variant]
+    d.device = device
+    return d, (mask, mu, ep)
+
+
+def topology_array(w, name: str) -> np.ndarray:
+    """Host-only integer topology (numbering, pattern of A, N_i, G_i columns)."""
+    d, keep = _desc(w)
+    n = C.c_int64(0)
+    which = L.INT_ARRAYS[name]
+    L.check(L.lib().mdd_topology_int_array(C.byref(d), which, None, 0, C.byref(n)))
+    out = np.empty(n.value, np.int64)
+    L.check(L.lib().mdd_topology_int_array(C.byref(d), which,
+                                           out.ctypes.data_as(C.POINTER(C.c_int64)), n.value,
+                                           C.byref(n)))
+    return out
+
+
+def _ptr(t) -> int:
+    """Device pointer of a contiguous float64 CUDA tensor."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
+            and t.is_contiguous()):
+        raise TypeError("expected a contiguous float64 CUDA tensor")
+    return t.data_ptr()
+
+
+class MaxwellDD:
+    """Handle of one set-up problem: ``MaxwellDD(workload)`` runs the device setup;
+    ``solve(f)`` runs PCG on the device."""
+
+    def __init__(self, w, coarse="snk", variant="as2", device=0, geneo=True):
+        self.w = w
+        d, keep = _desc(w, coarse, variant, device, geneo)
+        h = C.c_void_p()
+        L.check(L.lib().mdd_setup(C.byref(d), C.byref(h)))
+        self._h = h
+        self.info = self._info()
+        self.n = int(self.info["n"])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().mdd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _info(self):
+        out = (C.c_int64 * len(L.INFO_NAMES))()
+        L.check(L.lib().mdd_info(self._h, out, len(L.INFO_NAMES)))
+        return dict(zip(L.INFO_NAMES, list(out)))
+
+    def int_array(self, name):
+        n = C.c_int64(0)
+        which = L.INT_ARRAYS[name]
+        L.check(L.lib().mdd_get_int_array(self._h, which, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.int64)
+        L.check(L.lib().mdd_get_int_array(self._h, which, out.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          n.value, C.byref(n)))
+        return out
+
+    def double_array(self, name):
+        n = C.c_int64(0)
+        which = L.DBL_ARRAYS[name]
+        L.check(L.lib().mdd_get_double_array(self._h, which, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        L.check(L.lib().mdd_get_double_array(self._h, which, out.ctypes.data_as(C.POINTER(C.c_double)),
+                                             n.value, C.byref(n)))
+        return out
+
+    def setup_times(self):
+        t = self.double_array("setup_times")
+        return {L.lib().mdd_phase_name(k).decode(): float(v) for k, v in enumerate(t)}
+
+    # ------------------------------------------------------------- device ops
+    def solve(self, f, x, tol=1e-8, maxit=1000):
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        rc = L.lib().mdd_solve(self._h, _ptr(f), _ptr(x), tol, maxit, C.byref(it), C.byref(rel))
+        if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
+            L.check(rc)
+        return it.value, rel.value, rc == L.MDD_OK
+
+    def solve_host(self, f: np.ndarray, tol=1e-8, maxit=1000):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        x = np.empty_like(f)
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        dp = C.POINTER(C.c_double)
+        rc = L.lib().mdd_solve_host(self._h, f.ctypes.data_as(dp), x.ctypes.data_as(dp), tol, maxit,
+                                    C.byref(it), C.byref(rel))
+        if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
+            L.check(rc)
+        return x, it.value, rel.value
+
+    def apply_preconditioner(self, r, z):
+        L.check(L.lib().mdd_apply_preconditioner(self._h, _ptr(r), _ptr(z)))
+
+    def apply_operator(self, x, y):
+        L.check(L.lib().mdd_apply_operator(self._h, _ptr(x), _ptr(y)))
+
+    def apply_local(self, r, z):
+        L.check(L.lib().mdd_apply_local(self._h, _ptr(r), _ptr(z)))
+
+    def apply_coarse(self, v, y):
+        L.check(L.lib().mdd_apply_coarse(self._h, _ptr(v), _ptr(y)))
+
+    def set_profiling(self, on=True):
+        L.check(L.lib().mdd_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self):
+        ms = (C.c_double * len(L.PROF_NAMES))()
+        ln = (C.c_int64 * len(L.PROF_NAMES))()
+        L.check(L.lib().mdd_profile(self._h, ms, ln, len(L.PROF_NAMES)))
+        return {k: (ms[i], ln[i]) for i, k in enumerate(L.PROF_NAMES)}
