@@ -1,0 +1,320 @@
+"""Benchmark of the solve phase: Schwarz-PCG DOF*iterations/s on B200.
+
+One "step" = one complete PCG solve  A x = f  to ||r|| <= 1e-8 ||f|| with the
+two-level additive Schwarz preconditioner M_AS,2 (SNK + GenEO coarse space,
+PAPER.md eq. 2.4 / §3 final display) -- every kernel of the hot path runs in
+libmaxwell_dd.so.  The one-time setup (assembly, local factorisations, GenEO
+GEVPs, E) runs on the device before the timed region and is reported
+separately under "setup_s".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
+
+N = 1: BASELINE.json configs[1] (c1: 32^3 cubes x 6 tets, 4^3 subdomains).
+N > 1 (torchrun, one rank per GPU): every rank solves its own replica of the
+workload (no data-path collective; the sharded solve is not built yet), value =
+all ranks' DOF*iterations / max-over-ranks time, "scaling": "weak".
+
+--impl reference times the CPU oracle (oracle/, fp64 numpy/scipy) on a bounded
+sample of the same recipe on rank 0; other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "Schwarz-PCG DOF*iterations/s"
+UNIT = "DOF*iter/s"
+TOL = 1e-8
+# the oracle sample: the c1 recipe (channels, contrast 1e4, gamma 1e-4, overlap 1,
+# threshold 0.1) on a 16^3 grid with 4^3 subdomains (setup untimed)
+CPU_SAMPLE = dict(n=16, p=4)
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--maxit", type=int, default=2000)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_oracle_sample(cfg, max_seconds=30.0, min_solves=1):
+    """Time the CPU oracle's solve phase (PCG to 1e-8 with M_AS,2) on the bounded
+    sample; returns (DOF*iter/s, description, cores)."""
+    import threadpoolctl  # noqa: F401  (scipy/numpy BLAS pools are used as they stand)
+    from oracle import solver as osolver
+    w = workloads.make(cfg, **CPU_SAMPLE) if cfg in ("c1",) else workloads.make(cfg)
+    t0 = time.perf_counter()
+    P = osolver.Problem(w)
+    setup = time.perf_counter() - t0
+    f = workloads.rhs(P.n, w.f_seed)
+    work, el, solves = 0.0, 0.0, 0
+    while solves < min_solves or el < max_seconds * 0.3:
+        t0 = time.perf_counter()
+        _, it, _ = P.solve(f, tol=TOL)
+        el += time.perf_counter() - t0
+        work += P.n * it
+        solves += 1
+        if el > max_seconds:
+            break
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    desc = (f"oracle (numpy/scipy fp64) PCG solve phase on the {cfg} recipe at "
+            f"{w.nx}^3 cubes, {w.px}^3 subdomains (n={P.n}, {it} iterations), {solves} solve(s); "
+            f"oracle setup {setup:.1f}s untimed")
+    return work / el, desc, cores, el / solves
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cfg = args.config
+    vals = []
+    desc = cores = None
+    for k in range(args.warmup + args.steps):
+        v, desc, cores, _ = cpu_oracle_sample(cfg, max_seconds=10.0)
+        if k >= args.warmup:
+            vals.append(v)
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg + "_oracle_sample", "recipe": cfg, **CPU_SAMPLE},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def main():
+    args = parse()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2311_18783_b200 import MaxwellDD
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = workloads.make(args.config)
+    t0 = time.perf_counter()
+    G = MaxwellDD(w, device=local)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream()
+    G.set_stream(stream)
+    n = G.n
+    f_host = workloads.rhs(n, w.f_seed + rank)
+    f = torch.as_tensor(f_host, device="cuda")
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def l2_flush():
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+
+    # ---- warm-up
+    iters = []
+    for _ in range(args.warmup):
+        l2_flush()
+        it, relres, ok = G.solve(f, x, tol=TOL, maxit=args.maxit)
+        assert ok, f"PCG did not converge (relres {relres})"
+        iters.append(it)
+
+    # ---- timed steps (device events on the library's stream, L2 flushed between steps)
+    G.set_profiling(True)
+    prof_acc = {}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    t_ms = 0.0
+    launches = 0
+    work = 0
+    for _ in range(args.steps):
+        l2_flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        it, relres, ok = G.solve(f, x, tol=TOL, maxit=args.maxit)
+        e1.record(stream)
+        e1.synchronize()
+        assert ok
+        t_ms += e0.elapsed_time(e1)
+        launches += G.last_launches()
+        work += n * it
+        for k, (ms, cnt) in G.profile().items():
+            a = prof_acc.setdefault(k, [0.0, 0])
+            a[0] += ms
+            a[1] += cnt
+        iters.append(it)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    G.set_profiling(False)
+    step_ms = t_ms / args.steps
+    # max over ranks
+    tt = torch.tensor([step_ms, float(work)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = tt.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        step_ms_max = float(tmax[0])
+        total_work = float(tt[1])
+    else:
+        step_ms_max = step_ms
+        total_work = float(work)
+    value = total_work / (step_ms_max * args.steps / 1e3)
+
+    # ---- e2e: host buffers through mdd_solve_host (H2D of f + D2H of x inside)
+    fp = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    fp.numpy()[:] = f_host
+    xp = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    e2e_ms, e2e_work = 0.0, 0
+    for _ in range(max(1, args.steps)):
+        l2_flush()
+        stream.synchronize()
+        t0 = time.perf_counter()
+        _, it, _ = G.solve_host_into(fp.numpy(), xp.numpy(), tol=TOL, maxit=args.maxit)
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+        e2e_work += n * it
+    e2e_val = e2e_work / (e2e_ms / 1e3)
+    if world > 1:
+        ev = torch.tensor([e2e_ms, float(e2e_work)], dtype=torch.float64, device="cuda")
+        em = ev.clone()
+        dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        e2e_val = float(ev[1]) / (float(em[0]) / 1e3)
+
+    info = G.info
+    roof = roofline(G, prof_acc, info)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n_dofs": n, "subdomains": info["nsub"],
+                   "n0_coarse": info["n0"], "geneo_vectors": info["ngeneo"],
+                   "iterations": iters[-1], "tol": TOL, "gamma": w.gamma,
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed between steps (256 MB write)"},
+        "iterations": iters[-1],
+        "sizes": info,
+        "setup_s": setup_s,
+        "setup_phases_s": G.setup_times(),
+        "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof_acc.items()},
+        "roofline": roof,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        v, desc, cores, _ = cpu_oracle_sample(args.config)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    G.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(G, prof, info):
+    """Dominant kernel class of the step and its achieved HBM bandwidth against
+    the measured copy bandwidth (MEASURED_PEAKS.json)."""
+    peak, src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+            src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    # algorithmic bytes of one preconditioner application
+    b = G.bytes_model()
+    name = "preconditioner M_AS,2 (local LDL^T sweeps + coarse + 2 SpMV)"
+    ms, cnt = prof.get("local_fwd", (0.0, 0))
+    if cnt == 0 or ms <= 0:
+        return None
+    achieved = b["precond"] / (ms / cnt / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_source": src,
+            "bytes_per_launch": b["precond"], "avg_launch_ms": ms / cnt}
+
+
+if __name__ == "__main__":
+    main()

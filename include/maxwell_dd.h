@@ -98,6 +98,12 @@ int mdd_solve(mdd_handle h, const double* f, double* x, double tol, int maxit, i
 int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int maxit,
                    int* iters, double* relres);
 
+/* Run all later device work of the handle on `stream` (a cudaStream_t of the
+ * handle's device, owned by the caller, which must outlive the handle or be
+ * replaced); NULL restores a private non-blocking stream.  Synchronises the
+ * previous stream first. */
+int mdd_set_stream(mdd_handle h, void* stream);
+
 /* z = M^{-1} r for the configured variant (eq. 2.3 / 2.4).  DEVICE pointers. */
 int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z);
 /* y = A x (CSR SpMV).  DEVICE pointers. */
@@ -127,6 +133,9 @@ enum {
   MDD_INFO_COARSE_LEVELS,
   MDD_INFO_NNZ_Z,
   MDD_INFO_KERNELS_PER_ITER, /* kernel launches per PCG iteration       */
+  MDD_INFO_LAST_LAUNCHES,   /* kernels launched by the last solve/apply call */
+  MDD_INFO_COARSE_PERTURBED,/* pivots of the Jacobi-scaled E raised to the static-pivot
+                               threshold 1e-14 (kappa(E) ~ 1/eps; 0 = exact LDL^T)   */
   MDD_INFO_COUNT
 };
 int mdd_info(mdd_handle h, int64_t* out, int count);

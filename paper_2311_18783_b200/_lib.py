@@ -20,7 +20,8 @@ VARIANT = {"as2": 0, "additive": 1, "as1": 2}
 INFO_NAMES = ["n", "nedges", "nfree_nodes", "nsub", "nnz_A", "nloc", "grad_candidates",
               "grad_rank", "ngeneo", "n0", "local_factor_nnz", "coarse_factor_nnz",
               "local_supernodes", "local_levels", "coarse_supernodes", "coarse_levels",
-              "nnz_Z", "kernels_per_iter"]
+              "nnz_Z", "kernels_per_iter", "last_launches",
+              "coarse_perturbed"]
 INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, "A_ptr": 4,
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
               "geneo_count": 10}
@@ -38,7 +39,8 @@ class SetupDesc(C.Structure):
 
 
 # every symbol include/maxwell_dd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_apply_preconditioner",
+EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_stream",
+           "mdd_apply_preconditioner",
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_info",
            "mdd_get_int_array", "mdd_topology_int_array", "mdd_get_double_array",
            "mdd_phase_name", "mdd_set_profiling", "mdd_profile", "mdd_last_error"]
@@ -57,6 +59,7 @@ def load() -> C.CDLL:
         "mdd_destroy": (None, [P]),
         "mdd_solve": (C.c_int, [P, P, P, C.c_double, C.c_int, C.POINTER(C.c_int), dp]),
         "mdd_solve_host": (C.c_int, [P, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp]),
+        "mdd_set_stream": (C.c_int, [P, P]),
         "mdd_apply_preconditioner": (C.c_int, [P, P, P]),
         "mdd_apply_operator": (C.c_int, [P, P, P]),
         "mdd_apply_local": (C.c_int, [P, P, P]),

@@ -36,6 +36,9 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// static-pivot threshold of the coarse LDL^T (unit-diagonal scaled E)
+const double kCoarsePivotTol = 1e-14;
+
 inline int nblk(int64_t n, int t) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
 
 // --------------------------------------------------- cuSPARSE SpGEMM helper
@@ -45,43 +48,75 @@ struct DevCsr {
   DBuf<double> val;
 };
 
-void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s) {
+// C = A B with cuSPARSE SpGEMM.  ALG1 (the default) needs workspace that grows
+// with the intermediate products and reports INSUFFICIENT_RESOURCES on the large
+// coarse products; then ALG2 and finally the chunked ALG3 are used.
+void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
+            const char* what) {
   CUSPARSE_CHECK(cusparseSetStream(H, s));
-  cusparseSpMatDescr_t a, b, c;
-  CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p,
-                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-  CUSPARSE_CHECK(cusparseCreateCsr(&b, B.rows, B.cols, B.nnz, B.ptr.p, B.idx.p, B.val.p,
-                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-  C.rows = A.rows; C.cols = B.cols;
-  C.ptr.alloc(C.rows + 1);
-  CUSPARSE_CHECK(cusparseCreateCsr(&c, C.rows, C.cols, 0, C.ptr.p, nullptr, nullptr,
-                                   CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-  cusparseSpGEMMDescr_t d;
-  CUSPARSE_CHECK(cusparseSpGEMM_createDescr(&d));
-  double one = 1.0, zero = 0.0;
-  auto op = CUSPARSE_OPERATION_NON_TRANSPOSE;
-  size_t b1 = 0, b2 = 0;
-  CUSPARSE_CHECK(cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                               CUSPARSE_SPGEMM_DEFAULT, d, &b1, nullptr));
-  DBuf<char> w1; w1.alloc(std::max<size_t>(b1, 1));
-  CUSPARSE_CHECK(cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                               CUSPARSE_SPGEMM_DEFAULT, d, &b1, w1.p));
-  CUSPARSE_CHECK(cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                        CUSPARSE_SPGEMM_DEFAULT, d, &b2, nullptr));
-  DBuf<char> w2; w2.alloc(std::max<size_t>(b2, 1));
-  CUSPARSE_CHECK(cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                        CUSPARSE_SPGEMM_DEFAULT, d, &b2, w2.p));
-  int64_t r_, c_, nnz;
-  CUSPARSE_CHECK(cusparseSpMatGetSize(c, &r_, &c_, &nnz));
-  C.nnz = nnz;
-  C.idx.alloc(std::max<int64_t>(nnz, 1));
-  C.val.alloc(std::max<int64_t>(nnz, 1));
-  CUSPARSE_CHECK(cusparseCsrSetPointers(c, C.ptr.p, C.idx.p, C.val.p));
-  CUSPARSE_CHECK(cusparseSpGEMM_copy(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                     CUSPARSE_SPGEMM_DEFAULT, d));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  cusparseSpGEMM_destroyDescr(d);
-  cusparseDestroySpMat(a); cusparseDestroySpMat(b); cusparseDestroySpMat(c);
+  const cusparseSpGEMMAlg_t algs[3] = {CUSPARSE_SPGEMM_DEFAULT, CUSPARSE_SPGEMM_ALG2,
+                                       CUSPARSE_SPGEMM_ALG3};
+  std::string errs;
+  for (int ai = 0; ai < 3; ++ai) {
+    const cusparseSpGEMMAlg_t alg = algs[ai];
+    cusparseSpMatDescr_t a, b, c;
+    CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p,
+                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+    CUSPARSE_CHECK(cusparseCreateCsr(&b, B.rows, B.cols, B.nnz, B.ptr.p, B.idx.p, B.val.p,
+                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+    C.rows = A.rows; C.cols = B.cols;
+    C.ptr.alloc(C.rows + 1);
+    CUSPARSE_CHECK(cusparseCreateCsr(&c, C.rows, C.cols, 0, C.ptr.p, nullptr, nullptr,
+                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
+    cusparseSpGEMMDescr_t d;
+    CUSPARSE_CHECK(cusparseSpGEMM_createDescr(&d));
+    double one = 1.0, zero = 0.0;
+    auto op = CUSPARSE_OPERATION_NON_TRANSPOSE;
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    DBuf<char> w1, w2, w3;
+    cusparseStatus_t st = cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
+                                                        alg, d, &b1, nullptr);
+    if (st == CUSPARSE_STATUS_SUCCESS) {
+      w1.alloc(std::max<size_t>(b1, 1));
+      st = cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b1, w1.p);
+    }
+    if (st == CUSPARSE_STATUS_SUCCESS && alg == CUSPARSE_SPGEMM_ALG3) {
+      st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
+                                         &b3, nullptr, nullptr);
+      if (st == CUSPARSE_STATUS_SUCCESS) {
+        w3.alloc(std::max<size_t>(b3, 1));
+        st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
+                                           &b3, w3.p, &b2);
+      }
+      w1.release();
+    } else if (st == CUSPARSE_STATUS_SUCCESS) {
+      st = cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b2, nullptr);
+    }
+    if (st == CUSPARSE_STATUS_SUCCESS) {
+      w2.alloc(std::max<size_t>(b2, 1));
+      st = cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b2, w2.p);
+    }
+    int64_t r_ = 0, c_ = 0, nnz = 0;
+    if (st == CUSPARSE_STATUS_SUCCESS) st = cusparseSpMatGetSize(c, &r_, &c_, &nnz);
+    if (st == CUSPARSE_STATUS_SUCCESS) {
+      C.nnz = nnz;
+      C.idx.alloc(std::max<int64_t>(nnz, 1));
+      C.val.alloc(std::max<int64_t>(nnz, 1));
+      st = cusparseCsrSetPointers(c, C.ptr.p, C.idx.p, C.val.p);
+    }
+    if (st == CUSPARSE_STATUS_SUCCESS)
+      st = cusparseSpGEMM_copy(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d);
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    cusparseSpGEMM_destroyDescr(d);
+    cusparseDestroySpMat(a); cusparseDestroySpMat(b); cusparseDestroySpMat(c);
+    if (st == CUSPARSE_STATUS_SUCCESS) return;
+    errs += " alg" + std::to_string(ai) + ":status " + std::to_string((int)st);
+    if (st != CUSPARSE_STATUS_INSUFFICIENT_RESOURCES && st != CUSPARSE_STATUS_NOT_SUPPORTED) break;
+  }
+  throw Error(1, std::string("cuSPARSE SpGEMM failed for ") + what + " (" + std::to_string(A.rows) +
+                     "x" + std::to_string(A.cols) + " nnz " + std::to_string(A.nnz) + " times " +
+                     std::to_string(B.rows) + "x" + std::to_string(B.cols) + " nnz " +
+                     std::to_string(B.nnz) + "):" + errs);
 }
 
 void transpose(cusparseHandle_t H, const DevCsr& A, DevCsr& T, cudaStream_t s) {
@@ -152,7 +187,7 @@ struct mdd_solver {
   DBuf<int64_t> Z_ptr, Zt_ptr;  // Z: n x n0 (cols = coarse positions); Zt: n0 x n
   DBuf<int32_t> Z_idx, Zt_idx;
   DBuf<double> Z_val, Zt_val;
-  int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0;
+  int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0, coarse_perturbed = 0;
   std::vector<int64_t> geneo_count;
   std::vector<double> geneo_lambda;
   // PCG work
@@ -162,6 +197,8 @@ struct mdd_solver {
   int nparts = 0;
   std::vector<double> setup_times;
   int64_t kernels_per_iter = 0;
+  int64_t launches = 0;         // kernels launched by the last solve / apply call
+  bool own_stream = true;
   bool profiling = false;
   double prof_ms[MDD_PROF_COUNT] = {0};
   int64_t prof_launch[MDD_PROF_COUNT] = {0};
@@ -172,7 +209,7 @@ struct mdd_solver {
     if (sp) cusparseDestroy(sp);
     if (profiling)
       for (auto& e : ev) cudaEventDestroy(e);
-    if (stream) cudaStreamDestroy(stream);
+    if (stream && own_stream) cudaStreamDestroy(stream);
   }
 
   // ------------------------------------------------------------ helpers
@@ -181,6 +218,7 @@ struct mdd_solver {
     int warps_per_block = 8;
     dev::k_spmv<<<nblk(rows, warps_per_block), 32 * warps_per_block, 0, stream>>>(
         rows, ptr, idx, val, in, out, dotw, part_, state.p);
+    launches += 1;
   }
   void applyA(const double* in, double* out) {
     spmv(A_ptr.p, A_idx.p, A_val.p, n, in, out);
@@ -189,6 +227,7 @@ struct mdd_solver {
     loc.forward(rr, gmap.p, xloc.p, stream);
     loc.backward(xloc.p, stream);
     dev::k_prolong<<<nblk(n, 256), 256, 0, stream>>>(n, pro_ptr.p, pro_pos.p, xloc.p, zz);
+    launches += 2 * loc.fp.nlevels + 1;
   }
   void apply_coarse(const double* v, double* y) {
     dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
@@ -197,6 +236,7 @@ struct mdd_solver {
     crs.backward(xc.p, stream);
     dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
                                                                          xc.p, y, state.p);
+    launches += 2 * crs.fp.nlevels + 2;
   }
   void apply_prec(const double* rr, double* zz) {
     int v = desc.variant;
@@ -208,6 +248,7 @@ struct mdd_solver {
       apply_local(rr, t4.p);
       apply_coarse(rr, t1.p);
       dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, t4.p, 1.0, t1.p, zz, state.p);
+      launches += 1;
       return;
     }
     // eq. (2.4): z = Q r + (I - Q A) M_AS (I - A Q) r
@@ -218,10 +259,12 @@ struct mdd_solver {
     applyA(t4.p, t2.p);                                            // t2 = A w
     apply_coarse(t2.p, t3.p);                                      // t3 = Q A w
     dev::k_combine3<<<nblk(n, 256), 256, 0, stream>>>(n, t1.p, t4.p, t3.p, zz, state.p);
+    launches += 2;  // axpby + combine3
   }
   void dot(const double* a, const double* b, int slot) {
     dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p);
     dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
+    launches += 2;
   }
 };
 
@@ -453,7 +496,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         Zit.rows = nc; Zit.cols = n; Zit.nnz = (int64_t)cdof.size();
         Zit.ptr.upload(tptr); Zit.idx.upload(tidx); Zit.val.upload(tval);
       }
-      spgemm(H->sp, Zit, Zi, G, s);
+      spgemm(H->sp, Zit, Zi, G, s, "gradient Gram Zint^T Zint");
       Csr gpat;
       std::vector<int64_t> gslot;
       download_sorted(G, gpat, gslot);
@@ -555,9 +598,19 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       Ad.idx.upload(H->Apat.idx);
       Ad.val.alloc(Ad.nnz);
       CUDA_CHECK(cudaMemcpyAsync(Ad.val.p, H->A_val.p, Ad.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      spgemm(H->sp, Ad, Z, W, s);
+      spgemm(H->sp, Ad, Z, W, s, "A Z");
       transpose(H->sp, Z, Zt, s);
-      spgemm(H->sp, Zt, W, E, s);
+      spgemm(H->sp, Zt, W, E, s, "Z^T (A Z)");
+      // Jacobi scaling E <- S E S, Z <- Z S (S = diag(E)^{-1/2}): the coarse operator
+      // Z E^{-1} Z^T is unchanged, the factorised matrix has a unit diagonal
+      DBuf<double> sc;
+      sc.alloc(nb);
+      dev::k_inv_sqrt_diag<<<nblk(nb, 256), 256, 0, s>>>((int)nb, E.ptr.p, E.idx.p, E.val.p, sc.p);
+      dev::k_scale_csr<<<nblk(nb, 256), 256, 0, s>>>((int)nb, E.ptr.p, E.idx.p, E.val.p, sc.p, sc.p);
+      dev::k_scale_csr<<<nblk(n, 256), 256, 0, s>>>(n, Z.ptr.p, Z.idx.p, Z.val.p, nullptr, sc.p);
+      dev::k_scale_csr<<<nblk(nb, 256), 256, 0, s>>>((int)nb, Zt.ptr.p, Zt.idx.p, Zt.val.p, sc.p, nullptr);
+      CUDA_CHECK(cudaGetLastError());
+      CUDA_CHECK(cudaStreamSynchronize(s));
     }
     Csr epat;
     std::vector<int64_t> eslot;
@@ -586,7 +639,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     std::vector<SymSystem> sys{SymSystem{&epat, exyz.data(), eslot.data()}};
     build_factor_plan(H->crs.fp, sys, 64);
     H->crs.upload();
-    H->crs.factor(E.val.p, 0, 0.0, nullptr, s);
+    H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);
     // hot-path copies of Z with columns relabelled to coarse positions
     {
       std::vector<int> zp(n + 1), zi(Z.nnz);
@@ -653,6 +706,7 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
   cudaStream_t s = H->stream;
   const int n = H->n;
   using namespace dev;
+  H->launches = 0;
   H->state.zero(s);
   H->S.zero(s);
   CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
@@ -686,6 +740,7 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
   H->apply_prec(H->r.p, H->z.p);
   mark(1);
   k_copy<<<nblk(n, 256), 256, 0, s>>>(n, H->z.p, H->p.p, H->state.p);
+  H->launches += 1;
   H->dot(H->r.p, H->z.p, S_RZ);
   int k = 0;
   bool converged = false;
@@ -699,6 +754,7 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
     k_update_xr<<<H->nparts, 256, 0, s>>>(n, x, H->r.p, H->p.p, H->q.p, H->S.p, H->part.p, H->state.p);
     k_reduce<<<1, 256, 0, s>>>(H->nparts, H->part.p, H->S.p + S_RR, H->state.p);
     k_scalar_step<<<1, 1, 0, s>>>(1, H->S.p, H->state.p, tol, k);
+    H->launches += 6;
     mark(4);
     CUDA_CHECK(cudaMemcpyAsync(H->state_host, H->state.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
@@ -712,6 +768,7 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
     H->dot(H->r.p, H->z.p, S_RZNEW);
     k_scalar_step<<<1, 1, 0, s>>>(2, H->S.p, H->state.p, tol, k);
     k_update_p<<<H->nparts, 256, 0, s>>>(n, H->p.p, H->z.p, H->S.p, H->state.p);
+    H->launches += 2;
     mark(7);
     if (prof) {
       acc(MDD_PROF_LOCAL_FWD, 5, 6);  // whole preconditioner (split below if needed)
@@ -785,6 +842,22 @@ int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int max
   });
 }
 
+int mdd_set_stream(mdd_handle h, void* stream) {
+  if (!h) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(h->device));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    if (h->own_stream) CUDA_CHECK(cudaStreamDestroy(h->stream));
+    if (stream) {
+      h->stream = (cudaStream_t)stream;
+      h->own_stream = false;
+    } else {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+  });
+}
+
 int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z) {
   if (!h || !r || !z) { g_err = "null argument"; return MDD_ERR_ARG; }
   return guard([&] {
@@ -847,6 +920,8 @@ int mdd_info(mdd_handle h, int64_t* out, int count) {
   v[MDD_INFO_COARSE_LEVELS] = h->has_coarse ? h->crs.fp.nlevels : 0;
   v[MDD_INFO_NNZ_Z] = h->nnzZ;
   v[MDD_INFO_KERNELS_PER_ITER] = 0;
+  v[MDD_INFO_LAST_LAUNCHES] = h->launches;
+  v[MDD_INFO_COARSE_PERTURBED] = h->coarse_perturbed;
   for (int k = 0; k < count && k < MDD_INFO_COUNT; ++k) out[k] = v[k];
   return MDD_OK;
 }

@@ -80,7 +80,7 @@ struct DevFactor {
   dev::PlanDev plan() const;
   void upload();
   // numeric multifrontal factorisation from a device value array `src`
-  void factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
+  int factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
   void forward(const double* b, const int32_t* gmap, double* x, cudaStream_t s) const;
   void backward(double* x, cudaStream_t s) const;
 };

@@ -65,7 +65,7 @@ void DevFactor::upload() {
   upd.alloc(std::max<int64_t>(fp.usize, 1));
 }
 
-void DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s) {
+int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s) {
   DBuf<double> fronts, umat;
   fronts.alloc(std::max<int64_t>(fp.fsize, 1));
   umat.alloc(std::max<int64_t>(fp.umsize, 1));
@@ -83,7 +83,9 @@ void DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped
   CUDA_CHECK(cudaStreamSynchronize(s));
   int e = 0;
   CUDA_CHECK(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (mode == 2) return e;
   MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");
+  return 0;
 }
 
 void DevFactor::forward(const double* b, const int32_t* gmap, double* x, cudaStream_t s) const {

@@ -140,6 +140,27 @@ __global__ void k_slot_sums(int64_t nslot, const int64_t* __restrict__ ptr, cons
   out[s] = k + gamma * m;
 }
 
+// s[r] = 1/sqrt(E_rr) for a CSR matrix with int32 pointers
+__global__ void k_inv_sqrt_diag(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                const double* __restrict__ val, double* __restrict__ s) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double d = 0.0;
+  for (int k = ptr[r]; k < ptr[r + 1]; ++k)
+    if (idx[k] == r) d = val[k];
+  s[r] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+}
+
+// val[k] *= (rs ? rs[row] : 1) * (cs ? cs[idx[k]] : 1)
+__global__ void k_scale_csr(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                            double* __restrict__ val, const double* __restrict__ rs,
+                            const double* __restrict__ cs) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double a = rs ? rs[r] : 1.0;
+  for (int k = ptr[r]; k < ptr[r + 1]; ++k) val[k] *= a * (cs ? cs[idx[k]] : 1.0);
+}
+
 // --------------------------------------------------- multifrontal LDL^T
 __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
                                   double* __restrict__ fronts, double* __restrict__ L,
@@ -171,7 +192,17 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
     const double d = Fj[j];
     bool drop = false;
     if (mode == 1) drop = !(d > tol);
-    else if (!(d > 0.0)) {
+    else if (mode == 2) {
+      // static pivoting: a pivot at or below tol (relative to the unit diagonal of
+      // the Jacobi-scaled matrix) is a rounding casualty of an SPD matrix with
+      // kappa ~ 1/eps; it is replaced by tol and counted
+      if (!(d > tol)) {
+        if (tid == 0) atomicAdd(err, 1);
+        __syncthreads();
+        if (tid == 0) Fj[j] = tol;
+        __syncthreads();
+      }
+    } else if (!(d > 0.0)) {
       if (tid == 0) atomicExch(err, 1);
       drop = true;
     }
@@ -184,11 +215,12 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
       __syncthreads();
       continue;
     }
-    const double rd = 1.0 / d;
+    const double dd = Fj[j];
+    const double rd = 1.0 / dd;
     for (int i = j + 1 + tid; i < nr; i += nt) Fj[i] *= rd;
     __syncthreads();
     for (int k = j + 1 + warp; k < nr; k += nw) {
-      const double lkd = Fj[k] * d;
+      const double lkd = Fj[k] * dd;
       double* Fk = F + (i64)k * nr;
       for (int i = k + lane; i < nr; i += 32) Fk[i] -= Fj[i] * lkd;
     }

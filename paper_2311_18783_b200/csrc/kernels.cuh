@@ -54,6 +54,12 @@ __global__ void k_slot_sums(int64_t nslot, const int64_t* __restrict__ ptr, cons
                             const double* __restrict__ Ke, const double* __restrict__ Me, double gamma,
                             double* __restrict__ out);
 
+__global__ void k_inv_sqrt_diag(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                const double* __restrict__ val, double* __restrict__ s);
+__global__ void k_scale_csr(int n, const int* __restrict__ ptr, const int* __restrict__ idx,
+                            double* __restrict__ val, const double* __restrict__ rs,
+                            const double* __restrict__ cs);
+
 // --------------------------------------------------- multifrontal LDL^T
 struct PlanDev {
   const i64* sn_col0;
@@ -75,7 +81,8 @@ struct PlanDev {
 };
 
 // mode 0: SPD (pivot <= 0 flags an error); mode 1: rank-revealing (pivot <= tol is
-// a dependent column: D^{-1} = 0, L column = 0, flagged in `dropped`)
+// a dependent column: D^{-1} = 0, L column = 0, flagged in `dropped`); mode 2:
+// static pivoting (pivot <= tol replaced by tol, counted in *err)
 __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
                                   double* __restrict__ fronts, double* __restrict__ L,
                                   double* __restrict__ dinv, double* __restrict__ umat, int mode,

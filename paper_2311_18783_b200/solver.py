@@ -121,6 +121,41 @@ class MaxwellDD:
             L.check(rc)
         return x, it.value, rel.value
 
+    def set_stream(self, stream):
+        """Run the handle's device work on a torch.cuda.Stream (or raw handle int);
+        None restores the library's private stream."""
+        raw = None if stream is None else int(getattr(stream, "cuda_stream", stream))
+        L.check(L.lib().mdd_set_stream(self._h, raw))
+
+    def last_launches(self):
+        return int(self._info()["last_launches"])
+
+    def solve_host_into(self, f: np.ndarray, x: np.ndarray, tol=1e-8, maxit=1000):
+        """mdd_solve_host on caller-owned (e.g. pinned) float64 host arrays."""
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        dp = C.POINTER(C.c_double)
+        rc = L.lib().mdd_solve_host(self._h, f.ctypes.data_as(dp), x.ctypes.data_as(dp), tol, maxit,
+                                    C.byref(it), C.byref(rel))
+        if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
+            L.check(rc)
+        return x, it.value, rel.value
+
+    def bytes_model(self):
+        """Algorithmic HBM bytes of the solve-phase operations:
+        every stored value / index the operation needs, read once, and every
+        output written once."""
+        i = self.info
+        n, nnzA, nloc = i["n"], i["nnz_A"], i["nloc"]
+        spmv = 12 * nnzA + 8 * (n + 1) + 16 * n
+        local = 2 * 8 * i["local_factor_nnz"] + 8 * nloc + 4 * nloc + 3 * 8 * nloc + 8 * n + 8 * n
+        coarse = (2 * 12 * i["nnz_Z"] + 2 * 8 * i["coarse_factor_nnz"] + 8 * i["n0"] + 16 * n) \
+            if i["n0"] else 0
+        vec = 8 * n * 4
+        precond = local + 2 * coarse + 2 * spmv + vec
+        return {"spmv": spmv, "local": local, "coarse": coarse, "precond": precond,
+                "iteration": precond + spmv + 8 * n * 7}
+
     def apply_preconditioner(self, r, z):
         L.check(L.lib().mdd_apply_preconditioner(self._h, _ptr(r), _ptr(z)))
 
