@@ -39,8 +39,8 @@ METRIC = "Schwarz-PCG DOF*iterations/s"
 UNIT = "DOF*iter/s"
 TOL = 1e-8
 # the oracle sample: the c1 recipe (channels, contrast 1e4, gamma 1e-4, overlap 1,
-# threshold 0.1) on a 16^3 grid with 4^3 subdomains (setup untimed)
-CPU_SAMPLE = dict(n=16, p=4)
+# threshold 0.1) on a 12^3 grid with 2^3 subdomains (setup untimed)
+CPU_SAMPLE = dict(n=12, p=2)
 
 
 def _env_int(k, d):

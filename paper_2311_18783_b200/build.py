@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmaxwell_dd.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "kernels.cu", "factor_driver.cu",
+SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
            "geneo.cu", "api.cu"]
 
 

@@ -80,15 +80,20 @@ void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cud
       w1.alloc(std::max<size_t>(b1, 1));
       st = cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b1, w1.p);
     }
-    if (st == CUSPARSE_STATUS_SUCCESS && alg == CUSPARSE_SPGEMM_ALG3) {
-      st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
-                                         &b3, nullptr, nullptr);
+    if (st == CUSPARSE_STATUS_SUCCESS && alg != CUSPARSE_SPGEMM_DEFAULT) {
+      // ALG2 / ALG3: the compute buffer size comes from estimateMemory; buffer 1
+      // stays alive until the copy
+      int64_t nprod = 0;
+      st = cusparseSpGEMM_getNumProducts(d, &nprod);
+      if (st == CUSPARSE_STATUS_SUCCESS)
+        st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
+                                           &b3, nullptr, nullptr);
       if (st == CUSPARSE_STATUS_SUCCESS) {
         w3.alloc(std::max<size_t>(b3, 1));
         st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
                                            &b3, w3.p, &b2);
+        w3.release();
       }
-      w1.release();
     } else if (st == CUSPARSE_STATUS_SUCCESS) {
       st = cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b2, nullptr);
     }
@@ -223,20 +228,19 @@ struct mdd_solver {
   void applyA(const double* in, double* out) {
     spmv(A_ptr.p, A_idx.p, A_val.p, n, in, out);
   }
+  // z = sum_i R_i^T A_i^{-1} R_i r: one persistent launch (gather, fwd, D^{-1}, bwd,
+  // prolongation)
   void apply_local(const double* rr, double* zz) {
-    loc.forward(rr, gmap.p, xloc.p, stream);
-    loc.backward(xloc.p, stream);
-    dev::k_prolong<<<nblk(n, 256), 256, 0, stream>>>(n, pro_ptr.p, pro_pos.p, xloc.p, zz);
-    launches += 2 * loc.fp.nlevels + 1;
+    loc.sweep(rr, gmap.p, zz, stream);
+    launches += 1;
   }
   void apply_coarse(const double* v, double* y) {
     dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
                                                                  Zt_val.p, v, xc.p, state.p);
-    crs.forward(nullptr, nullptr, xc.p, stream);
-    crs.backward(xc.p, stream);
+    crs.sweep(xc.p, nullptr, nullptr, stream);
     dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
-                                                                         xc.p, y, state.p);
-    launches += 2 * crs.fp.nlevels + 2;
+                                                                         crs.xb.p, y, state.p);
+    launches += 3;
   }
   void apply_prec(const double* rr, double* zz) {
     int v = desc.variant;
@@ -260,6 +264,10 @@ struct mdd_solver {
     apply_coarse(t2.p, t3.p);                                      // t3 = Q A w
     dev::k_combine3<<<nblk(n, 256), 256, 0, stream>>>(n, t1.p, t4.p, t3.p, zz, state.p);
     launches += 2;  // axpby + combine3
+  }
+  void check_aborts() {
+    loc.check_abort(stream);
+    if (has_coarse) crs.check_abort(stream);
   }
   void dot(const double* a, const double* b, int slot) {
     dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p);
@@ -362,7 +370,6 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     std::vector<SymSystem> sys(nsub);
     for (int i = 0; i < nsub; ++i) sys[i] = SymSystem{&lpat[i], lxyz[i].data(), lslot[i].data()};
     build_factor_plan(H->loc.fp, sys, 64);
-    H->loc.upload();
     // position -> global dof, global dof -> positions (subdomain order)
     const FactorPlan& fp = H->loc.fp;
     std::vector<int32_t> gm(fp.ntot);
@@ -381,6 +388,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         pos[cur[H->dec.sub_dofs[i][k]]++] = fp.iperm_global[fp.sys_off[i] + k];
     H->pro_ptr.upload(pp);
     H->pro_pos.upload(pos);
+    H->loc.upload(n, H->pro_ptr.p, H->pro_pos.p);
   }
   H->setup_times[PH_LOCAL_SYMBOLIC] = now_s() - t0;
   t0 = now_s();
@@ -606,6 +614,12 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       DBuf<double> sc;
       sc.alloc(nb);
       dev::k_inv_sqrt_diag<<<nblk(nb, 256), 256, 0, s>>>((int)nb, E.ptr.p, E.idx.p, E.val.p, sc.p);
+      {
+        std::vector<double> hs = sc.download();
+        for (int64_t c = 0; c < nb; ++c)
+          MDD_REQUIRE(hs[c] > 0.0 && std::isfinite(hs[c]), 5,
+                      "coarse matrix E has a nonpositive diagonal entry (column " + std::to_string(c) + ")");
+      }
       dev::k_scale_csr<<<nblk(nb, 256), 256, 0, s>>>((int)nb, E.ptr.p, E.idx.p, E.val.p, sc.p, sc.p);
       dev::k_scale_csr<<<nblk(n, 256), 256, 0, s>>>(n, Z.ptr.p, Z.idx.p, Z.val.p, nullptr, sc.p);
       dev::k_scale_csr<<<nblk(nb, 256), 256, 0, s>>>((int)nb, Zt.ptr.p, Zt.idx.p, Zt.val.p, sc.p, nullptr);
@@ -636,7 +650,12 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     }
     H->setup_times[PH_COARSE_E] = now_s() - t0;
     t0 = now_s();
-    std::vector<SymSystem> sys{SymSystem{&epat, exyz.data(), eslot.data()}};
+    // GenEO columns (dense support on a whole subdomain) are eliminated last
+    std::vector<uint8_t> elast(nb, 0);
+    for (int64_t c = H->grad_rank; c < nb; ++c) elast[c] = 1;
+    SymSystem esys{&epat, exyz.data(), eslot.data()};
+    esys.last = elast.data();
+    std::vector<SymSystem> sys{esys};
     build_factor_plan(H->crs.fp, sys, 64);
     H->crs.upload();
     H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);
@@ -778,6 +797,7 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
   CUDA_CHECK(cudaGetLastError());
   CUDA_CHECK(cudaMemcpyAsync(hs.data(), H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  H->check_aborts();
   *iters = converged ? H->state_host[1] : maxit;
   *relres = hs[S_REL];
   if (!converged) throw Error(MDD_ERR_NOCONV, "PCG did not converge within maxit");
@@ -865,6 +885,7 @@ int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z) {
     h->apply_prec(r, z);
     CUDA_CHECK(cudaStreamSynchronize(h->stream));
     CUDA_CHECK(cudaGetLastError());
+    h->check_aborts();
   });
 }
 
@@ -885,6 +906,7 @@ int mdd_apply_local(mdd_handle h, const double* r, double* z) {
     h->apply_local(r, z);
     CUDA_CHECK(cudaStreamSynchronize(h->stream));
     CUDA_CHECK(cudaGetLastError());
+    h->check_aborts();
   });
 }
 
@@ -896,6 +918,7 @@ int mdd_apply_coarse(mdd_handle h, const double* v, double* y) {
     h->apply_coarse(v, y);
     CUDA_CHECK(cudaStreamSynchronize(h->stream));
     CUDA_CHECK(cudaGetLastError());
+    h->check_aborts();
   });
 }
 

@@ -95,6 +95,7 @@ struct SymSystem {
   const Csr* pat;                       // full symmetric pattern (both triangles), local indices
   const int32_t* xyz2;                  // 3 ints per unknown: doubled lattice coordinates
   const i64* val_slot;                  // per pattern entry: index of its value in the source array
+  const uint8_t* last = nullptr;        // optional: unknowns ordered after the nested dissection
 };
 
 void build_factor_plan(FactorPlan& fp, const std::vector<SymSystem>& systems, int leaf_size);

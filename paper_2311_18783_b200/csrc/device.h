@@ -69,20 +69,32 @@ struct DBuf {
   }
 };
 
-// A FactorPlan on the device plus its numeric factor.
+// A FactorPlan on the device plus its numeric factor and its sweep schedule.
 struct DevFactor {
   FactorPlan fp;
   DBuf<int64_t> col0, rowptr, offrows, lptr, uptr, fptr, umptr, child_ptr, asm_ptr, asm_src;
-  DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn;
-  DBuf<double> L, dinv, upd;
-  std::vector<int> fwd_smem, bwd_smem;  // bytes per level
-  int threads = 128;
+  DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn, parent;
+  DBuf<double> L, dinv, upd, xf, xb;
+  // persistent sweep (sweep.cu)
+  DBuf<int4> tasks;
+  DBuf<int> nbf, nbb;
+  DBuf<unsigned long long> fwd_cnt, bwd_cnt, ctl;
+  int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, sweep_smem = 0, sweep_grid = 0;
+  const int64_t* pro_ptr = nullptr;
+  const int32_t* pro_pos = nullptr;
   dev::PlanDev plan() const;
-  void upload();
+  // prolong_n > 0 appends prolongation chunks over prolong_n global dofs
+  void upload(int prolong_n = 0, const int64_t* pro_ptr_dev = nullptr,
+              const int32_t* pro_pos_dev = nullptr);
   // numeric multifrontal factorisation from a device value array `src`
   int factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
-  void forward(const double* b, const int32_t* gmap, double* x, cudaStream_t s) const;
-  void backward(double* x, cudaStream_t s) const;
+  // x = A^{-1} b in one persistent launch.  b is gathered through gmap (positions
+  // -> source index) when gmap != NULL; with `out` the result is prolongated to
+  // out[e] = sum of its copies (needs upload(prolong_n > 0)), else it stays in xb
+  // (positions).
+  void sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s) const;
+  // throws if a sweep aborted (spin timeout); resets the schedule state
+  void check_abort(cudaStream_t s);
 };
 
 }  // namespace mdd

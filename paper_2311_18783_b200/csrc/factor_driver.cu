@@ -27,7 +27,14 @@ dev::PlanDev DevFactor::plan() const {
   return P;
 }
 
-void DevFactor::upload() {
+namespace {
+// tasks of roughly kTaskEntries panel entries (~192 KB) so top-of-tree supernodes
+// spread over several SMs while leaves stay one task each
+constexpr int64_t kTaskEntries = 32768;
+constexpr int kProlongChunk = 2048;
+}  // namespace
+
+void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t* pro_pos_dev) {
   col0.upload(fp.sn_col0);
   ncol.upload(fp.sn_ncol);
   noff.upload(fp.sn_noff);
@@ -44,25 +51,113 @@ void DevFactor::upload() {
   asm_src.upload(fp.asm_src);
   asm_pos.upload(fp.asm_pos);
   level_sn.upload(fp.level_sn);
-  fwd_smem.assign(fp.nlevels, 0);
-  bwd_smem.assign(fp.nlevels, 0);
-  for (int l = 0; l < fp.nlevels; ++l)
-    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-      int g = fp.level_sn[k];
-      int nc = fp.sn_ncol[g], no = fp.sn_noff[g];
-      fwd_smem[l] = std::max(fwd_smem[l], (int)((nc + no + nc) * sizeof(double)));
-      bwd_smem[l] = std::max(bwd_smem[l], (int)((no + nc) * sizeof(double)));
-    }
-  int mx = 0;
-  for (int l = 0; l < fp.nlevels; ++l) mx = std::max(mx, std::max(fwd_smem[l], bwd_smem[l]));
-  MDD_REQUIRE(mx <= 227 * 1024, 5, "supernode too large for shared-memory staging");
-  if (mx > 48 * 1024) {
-    CUDA_CHECK(cudaFuncSetAttribute(dev::k_fwd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    CUDA_CHECK(cudaFuncSetAttribute(dev::k_bwd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  }
+  parent.upload(fp.sn_parent);
   L.alloc(fp.lsize);
   dinv.alloc(fp.ntot);
   upd.alloc(std::max<int64_t>(fp.usize, 1));
+  xf.alloc(std::max<int64_t>(fp.ntot, 1));
+  xb.alloc(std::max<int64_t>(fp.ntot, 1));
+  // ---- sweep schedule
+  std::vector<int4> tk;
+  std::vector<int> vf(fp.nsn), vb(fp.nsn);
+  int smem_d = 1;
+  for (int l = 0; l < fp.nlevels; ++l)
+    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+      const int g = fp.level_sn[k];
+      const int nc = fp.sn_ncol[g], no = fp.sn_noff[g], nr = nc + no;
+      const int64_t ent = (int64_t)nc * (nc + 1) / 2 + (int64_t)nc * no;
+      int rb = nr;
+      if (nr > dev::kSweepThreads || ent > kTaskEntries) {
+        rb = (int)std::min<int64_t>(dev::kSweepThreads, std::max<int64_t>(32, kTaskEntries / nc));
+        rb = rb / 32 * 32;
+      }
+      int cnt = 0;
+      for (int r0 = 0; r0 < nr; r0 += rb, ++cnt) tk.push_back(make_int4(0, g, r0, std::min(nr, r0 + rb)));
+      vf[g] = cnt;
+      smem_d = std::max(smem_d, nc + std::min(nr, rb) + dev::kSweepThreads);
+    }
+  ntasks_noprolong = 0;
+  total_bwd = 0;
+  for (int l = fp.nlevels - 1; l >= 0; --l)
+    for (int k = fp.level_ptr[l + 1] - 1; k >= fp.level_ptr[l]; --k) {
+      const int g = fp.level_sn[k];
+      const int nc = fp.sn_ncol[g], no = fp.sn_noff[g], nr = nc + no;
+      const int64_t ent = (int64_t)nc * (nc + 1) / 2 + (int64_t)nc * no;
+      int cb = nc;
+      if (ent > kTaskEntries) cb = (int)std::max<int64_t>(16, kTaskEntries / nr / 16 * 16);
+      int cnt = 0;
+      for (int c0 = 0; c0 < nc; c0 += cb, ++cnt) tk.push_back(make_int4(1, g, c0, std::min(nc, c0 + cb)));
+      vb[g] = cnt;
+      total_bwd += cnt;
+      smem_d = std::max(smem_d, nr + (dev::kSweepThreads / 32) * 16);
+    }
+  ntasks_noprolong = (int)tk.size();
+  if (prolong_n > 0) {
+    for (int e0 = 0; e0 < prolong_n; e0 += kProlongChunk)
+      tk.push_back(make_int4(2, 0, e0, std::min(prolong_n, e0 + kProlongChunk)));
+    pro_ptr = pro_ptr_dev;
+    pro_pos = pro_pos_dev;
+  }
+  ntasks = (int)tk.size();
+  tasks.upload(tk);
+  nbf.upload(vf);
+  nbb.upload(vb);
+  fwd_cnt.alloc(std::max(fp.nsn, 1));
+  bwd_cnt.alloc(std::max(fp.nsn, 1));
+  ctl.alloc(dev::SW_COUNT);
+  CUDA_CHECK(cudaMemset(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long)));
+  CUDA_CHECK(cudaMemset(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long)));
+  CUDA_CHECK(cudaMemset(ctl.p, 0, ctl.n * sizeof(unsigned long long)));
+  CUDA_CHECK(cudaDeviceSynchronize());
+  sweep_smem = smem_d * (int)sizeof(double);
+  MDD_REQUIRE(sweep_smem <= 200 * 1024, 5, "supernode too large for shared-memory staging");
+  if (sweep_smem > 48 * 1024)
+    CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem));
+  int dev_id = 0, nsm = 0, per_sm = 0;
+  CUDA_CHECK(cudaGetDevice(&dev_id));
+  CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, sweep_smem));
+  MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
+  sweep_grid = nsm * per_sm;
+}
+
+void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s) const {
+  dev::SweepDev S;
+  S.P = plan();
+  S.L = L.p;
+  S.dinv = dinv.p;
+  S.tasks = tasks.p;
+  S.ntasks = out ? ntasks : ntasks_noprolong;
+  S.total_bwd = total_bwd;
+  S.nbf = nbf.p;
+  S.nbb = nbb.p;
+  S.parent = parent.p;
+  S.fwd_cnt = fwd_cnt.p;
+  S.bwd_cnt = bwd_cnt.p;
+  S.ctl = ctl.p;
+  S.upd = upd.p;
+  S.xf = xf.p;
+  S.xb = xb.p;
+  S.b = b;
+  S.gmap = gmap;
+  S.pro_ptr = pro_ptr;
+  S.pro_pos = pro_pos;
+  S.out = out;
+  const int grid = std::max(1, std::min(sweep_grid, S.ntasks));
+  dev::k_sweep<<<grid, dev::kSweepThreads, sweep_smem, s>>>(S);
+}
+
+void DevFactor::check_abort(cudaStream_t s) {
+  unsigned long long ab = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&ab, ctl.p + dev::SW_ABORT, sizeof(ab), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  if (ab) {
+    CUDA_CHECK(cudaMemsetAsync(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long), s));
+    CUDA_CHECK(cudaMemsetAsync(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long), s));
+    CUDA_CHECK(cudaMemsetAsync(ctl.p, 0, ctl.n * sizeof(unsigned long long), s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    throw Error(5, "supernodal sweep aborted (dependency wait timed out)");
+  }
 }
 
 int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s) {
@@ -86,22 +181,6 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
   if (mode == 2) return e;
   MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");
   return 0;
-}
-
-void DevFactor::forward(const double* b, const int32_t* gmap, double* x, cudaStream_t s) const {
-  dev::PlanDev P = plan();
-  for (int l = 0; l < fp.nlevels; ++l) {
-    int cnt = fp.level_ptr[l + 1] - fp.level_ptr[l];
-    dev::k_fwd_level<<<cnt, threads, fwd_smem[l], s>>>(P, fp.level_ptr[l], L.p, dinv.p, b, gmap, x, upd.p);
-  }
-}
-
-void DevFactor::backward(double* x, cudaStream_t s) const {
-  dev::PlanDev P = plan();
-  for (int l = fp.nlevels - 1; l >= 0; --l) {
-    int cnt = fp.level_ptr[l + 1] - fp.level_ptr[l];
-    dev::k_bwd_level<<<cnt, threads, bwd_smem[l], s>>>(P, fp.level_ptr[l], L.p, x);
-  }
 }
 
 }  // namespace mdd

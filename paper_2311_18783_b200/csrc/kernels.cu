@@ -148,7 +148,7 @@ __global__ void k_inv_sqrt_diag(int n, const int* __restrict__ ptr, const int* _
   double d = 0.0;
   for (int k = ptr[r]; k < ptr[r + 1]; ++k)
     if (idx[k] == r) d = val[k];
-  s[r] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+  s[r] = d > 0.0 ? 1.0 / sqrt(d) : -1.0;  // -1 flags a missing / nonpositive diagonal
 }
 
 // val[k] *= (rs ? rs[row] : 1) * (cs ? cs[idx[k]] : 1)
@@ -253,77 +253,12 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
     }
     __syncthreads();
   }
-}
-
-// -------------------------------------------- supernodal triangular solves
-// CTA variant: one CTA per supernode.  Dynamic smem: t[nr] | y[nc].
-__global__ void k_fwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
-                            const double* __restrict__ dinv, const double* __restrict__ b,
-                            const int32_t* __restrict__ gmap, double* __restrict__ x,
-                            double* __restrict__ upd) {
-  extern __shared__ double sm[];
-  const int g = P.level_sn[level_begin + blockIdx.x];
-  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
-  const i64 col0 = P.sn_col0[g];
-  const double* __restrict__ Lp = L + P.sn_lptr[g];
-  double* t = sm;
-  double* y = sm + nr;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int k = tid; k < nc; k += nt) t[k] = gmap ? b[gmap[col0 + k]] : x[col0 + k];
-  for (int k = tid; k < no; k += nt) t[nc + k] = 0.0;
-  __syncthreads();
-  for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
-    const int c = P.child_list[ci];
-    const int noc = P.sn_noff[c];
-    const double* u = upd + P.sn_uptr[c];
-    const int* rm = P.relmap + P.sn_rowptr[c];
-    for (int a = tid; a < noc; a += nt) t[rm[a]] += u[a];
-    __syncthreads();
-  }
-  for (int i = tid; i < nc; i += nt) {
+  // partitioned-inverse off block: M21 = L21 L11^{-1} (sweep.cu), from F's L21
+  for (i64 k = tid; k < (i64)nc * no; k += nt) {
+    const int j = (int)(k / no), i = nc + (int)(k % no);
     double s = 0.0;
-    for (int j = 0; j <= i; ++j) s += Lp[(i64)j * nr + i] * t[j];
-    y[i] = s;
-  }
-  __syncthreads();
-  for (int i = tid; i < nc; i += nt) x[col0 + i] = dinv[col0 + i] * y[i];
-  double* uo = upd + P.sn_uptr[g];
-  for (int i = nc + tid; i < nr; i += nt) {
-    double s = t[i];
-    for (int j = 0; j < nc; ++j) s -= Lp[(i64)j * nr + i] * y[j];
-    uo[i - nc] = s;
-  }
-}
-
-// Backward: v = x_c - L21^T x_off ; x_c = Linv11^T v.  Warps over columns.
-__global__ void k_bwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
-                            double* __restrict__ x) {
-  extern __shared__ double sm[];
-  const int g = P.level_sn[level_begin + blockIdx.x];
-  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
-  const i64 col0 = P.sn_col0[g];
-  const double* __restrict__ Lp = L + P.sn_lptr[g];
-  const i64* rows = P.offrows + P.sn_rowptr[g];
-  double* xo = sm;        // no
-  double* v = sm + no;    // nc
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  for (int k = tid; k < no; k += nt) xo[k] = x[rows[k]];
-  __syncthreads();
-  for (int i = warp; i < nc; i += nw) {
-    const double* col = Lp + (i64)i * nr + nc;
-    double s = 0.0;
-    for (int k = lane; k < no; k += 32) s += col[k] * xo[k];
-    s = warp_sum(s);
-    if (lane == 0) v[i] = x[col0 + i] - s;
-  }
-  __syncthreads();
-  for (int i = warp; i < nc; i += nw) {
-    const double* col = Lp + (i64)i * nr;
-    double s = 0.0;
-    for (int k = i + lane; k < nc; k += 32) s += col[k] * v[k];
-    s = warp_sum(s);
-    if (lane == 0) x[col0 + i] = s;
+    for (int q = j; q < nc; ++q) s += F[(i64)q * nr + i] * Lp[(i64)j * nr + q];
+    Lp[(i64)j * nr + i] = s;
   }
 }
 

@@ -88,17 +88,34 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
                                   double* __restrict__ dinv, double* __restrict__ umat, int mode,
                                   double tol, uint8_t* __restrict__ dropped, int* __restrict__ err);
 
-// -------------------------------------------- supernodal triangular solves
-// Forward (L y = b, multifrontal extend-add of child update vectors) and
-// diagonal (D^{-1}); one CTA per supernode of the level.  If gmap != NULL the
-// right-hand side is gathered b[gmap[pos]] (fused restriction R_i), else x[pos].
-__global__ void k_fwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
-                            const double* __restrict__ dinv, const double* __restrict__ b,
-                            const int32_t* __restrict__ gmap, double* __restrict__ x,
-                            double* __restrict__ upd);
-// Backward (L^T x = y) from the roots down.
-__global__ void k_bwd_level(PlanDev P, int level_begin, const double* __restrict__ L,
-                            double* __restrict__ x);
+// -------------------------------------------- supernodal triangular sweeps
+// (sweep.cu) control words of a persistent sweep
+enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_COUNT };
+constexpr int kSweepThreads = 256;
+
+struct SweepDev {
+  PlanDev P;
+  const double* L;               // P-form panels
+  const double* dinv;
+  const int4* tasks;             // {type 0 fwd / 1 bwd / 2 prolong, supernode, lo, hi}
+  int ntasks;
+  int total_bwd;                 // bwd tasks per launch
+  const int* nbf;                // fwd tasks per supernode
+  const int* nbb;                // bwd tasks per supernode
+  const int* parent;             // supernode parent (-1 root)
+  unsigned long long* fwd_cnt;   // cumulative completion counters
+  unsigned long long* bwd_cnt;
+  unsigned long long* ctl;       // SW_* words
+  double* upd;                   // update vectors (noff per supernode)
+  double* xf;                    // forward result z (positions)
+  double* xb;                    // solution (positions)
+  const double* b;               // right-hand side: b[gmap[pos]] or b[pos]
+  const int32_t* gmap;
+  const int64_t* pro_ptr;        // prolongation (global dof -> positions)
+  const int32_t* pro_pos;
+  double* out;                   // prolongation target (global)
+};
+__global__ void k_sweep(SweepDev S);
 
 // prolongation sum_i R_i^T x_i: out[e] = sum over the copies of dof e (fixed order)
 __global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,

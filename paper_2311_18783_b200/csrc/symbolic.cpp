@@ -130,9 +130,12 @@ void analyse_one(Sys1& s, const SymSystem& sys, int leaf) {
   NDWork w;
   w.pat = &A; w.xyz2 = sys.xyz2; w.leaf = leaf;
   w.side.assign(n, -1);
-  std::vector<int32_t> V(n);
-  std::iota(V.begin(), V.end(), 0);
+  std::vector<int32_t> V, tail;
+  for (int v = 0; v < n; ++v) (sys.last && sys.last[v] ? tail : V).push_back(v);
   nd_rec(w, V);
+  // flagged unknowns (e.g. dense-support coarse columns) close the order, so their
+  // coupling never creates a clique inside the dissection
+  w.order.insert(w.order.end(), tail.begin(), tail.end());
   MDD_REQUIRE((int)w.order.size() == n, 5, "nested dissection lost vertices");
   std::vector<int32_t> perm = w.order, iperm(n);
   // etree + postorder, twice (the second pass is a no-op relabel check)
