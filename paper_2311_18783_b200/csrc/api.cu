@@ -208,8 +208,23 @@ struct mdd_solver {
   double prof_ms[MDD_PROF_COUNT] = {0};
   int64_t prof_launch[MDD_PROF_COUNT] = {0};
   cudaEvent_t ev[16];
+  // CUDA graph of the whole solve: prologue + device-side WHILE loop over iterations
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int64_t launches_prologue = 0, launches_body = 0;
+  double* host_S = nullptr;     // pinned staging of S / state
+  int* host_state = nullptr;
+
+  void drop_graph() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+    graph_stream = nullptr;
+  }
 
   ~mdd_solver() {
+    drop_graph();
+    if (host_S) cudaFreeHost(host_S);
+    if (host_state) cudaFreeHost(host_state);
     if (state_host) cudaFreeHost(state_host);
     if (sp) cusparseDestroy(sp);
     if (profiling)
@@ -231,13 +246,13 @@ struct mdd_solver {
   // z = sum_i R_i^T A_i^{-1} R_i r: one persistent launch (gather, fwd, D^{-1}, bwd,
   // prolongation)
   void apply_local(const double* rr, double* zz) {
-    loc.sweep(rr, gmap.p, zz, stream);
+    loc.sweep(rr, gmap.p, zz, stream, state.p);
     launches += 1;
   }
   void apply_coarse(const double* v, double* y) {
     dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
                                                                  Zt_val.p, v, xc.p, state.p);
-    crs.sweep(xc.p, nullptr, nullptr, stream);
+    crs.sweep(xc.p, nullptr, nullptr, stream, state.p);
     dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
                                                                          crs.xb.p, y, state.p);
     launches += 3;
@@ -273,6 +288,86 @@ struct mdd_solver {
     dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p);
     dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
     launches += 2;
+  }
+  void scalar(int op) {
+    dev::k_scalar_step<<<1, 1, 0, stream>>>(op, S.p, state.p);
+    launches += 1;
+  }
+  // ---------------------------------------------------------------- PCG
+  // prologue (x = 0 and r = f staged by the host): ||f||, z = M r, p = z, rz
+  void enqueue_prologue() {
+    dot(r.p, r.p, dev::S_RR);
+    scalar(3);
+    apply_prec(r.p, z.p);
+    dev::k_copy<<<nblk(n, 256), 256, 0, stream>>>(n, z.p, p.p, state.p);
+    launches += 1;
+    dot(r.p, z.p, dev::S_RZ);
+  }
+  // one PCG iteration; every kernel is a no-op once state[ST_STOP] is set.
+  // marks: optional event indices for the eager profiling path
+  void enqueue_body(const std::function<void(int)>& mark) {
+    const int blocks = nblk(n, 8);
+    if (mark) mark(2);
+    dev::k_spmv<<<blocks, 256, 0, stream>>>(n, A_ptr.p, A_idx.p, A_val.p, p.p, q.p, p.p, part.p, state.p);
+    launches += 1;
+    if (mark) mark(3);
+    dev::k_reduce<<<1, 256, 0, stream>>>(blocks, part.p, S.p + dev::S_PQ, state.p);
+    launches += 1;
+    scalar(0);
+    dev::k_update_xr<<<nparts, 256, 0, stream>>>(n, x.p, r.p, p.p, q.p, S.p, part.p, state.p);
+    dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + dev::S_RR, state.p);
+    launches += 2;
+    scalar(1);
+    if (mark) mark(4);
+    apply_prec(r.p, z.p);
+    if (mark) mark(5);
+    dot(r.p, z.p, dev::S_RZNEW);
+    scalar(2);
+    dev::k_update_p<<<nparts, 256, 0, stream>>>(n, p.p, z.p, S.p, state.p);
+    launches += 1;
+    if (mark) mark(6);
+  }
+  // graph: prologue -> WHILE(state not stopped) { body ; k_loop_cond }
+  void build_graph() {
+    drop_graph();
+    cudaGraph_t g;
+    CUDA_CHECK(cudaGraphCreate(&g, 0));
+    launches = 0;
+    CUDA_CHECK(cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_prologue();
+    CUDA_CHECK(cudaStreamEndCapture(stream, &g));
+    launches_prologue = launches;
+    // sinks of the prologue
+    size_t nn = 0, ne = 0;
+    CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    CUDA_CHECK(cudaGraphGetEdges(g, nullptr, nullptr, &ne));
+    std::vector<cudaGraphNode_t> from(ne), to(ne);
+    if (ne) CUDA_CHECK(cudaGraphGetEdges(g, from.data(), to.data(), &ne));
+    std::vector<cudaGraphNode_t> sinks;
+    for (auto nd : nodes)
+      if (std::find(from.begin(), from.end(), nd) == from.end()) sinks.push_back(nd);
+    cudaGraphConditionalHandle h;
+    CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    CUDA_CHECK(cudaGraphAddNode(&cn, g, sinks.data(), sinks.size(), &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    launches = 0;
+    CUDA_CHECK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_body(nullptr);
+    dev::k_loop_cond<<<1, 1, 0, stream>>>(h, state.p);
+    launches += 1;
+    CUDA_CHECK(cudaStreamEndCapture(stream, &body));
+    launches_body = launches;
+    CUDA_CHECK(cudaGraphInstantiate(&graph_exec, g, 0));
+    CUDA_CHECK(cudaGraphDestroy(g));
+    graph_stream = stream;
   }
 };
 
@@ -370,6 +465,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     std::vector<SymSystem> sys(nsub);
     for (int i = 0; i < nsub; ++i) sys[i] = SymSystem{&lpat[i], lxyz[i].data(), lslot[i].data()};
     build_factor_plan(H->loc.fp, sys, 64);
+    H->loc.name = "local";
     // position -> global dof, global dof -> positions (subdomain order)
     const FactorPlan& fp = H->loc.fp;
     std::vector<int32_t> gm(fp.ntot);
@@ -657,6 +753,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     esys.last = elast.data();
     std::vector<SymSystem> sys{esys};
     build_factor_plan(H->crs.fp, sys, 64);
+    H->crs.name = "coarse";
     H->crs.upload();
     H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);
     // hot-path copies of Z with columns relabelled to coarse positions
@@ -712,95 +809,77 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
   H->S.alloc(dev::S_COUNT);
   H->nparts = 4 * 148;
   H->part.alloc(std::max<int64_t>(H->nparts, nblk(n, 8)) + 8);
-  H->state.alloc(4);
+  H->state.alloc(dev::ST_COUNT);
   H->state.zero(s);
-  CUDA_CHECK(cudaMallocHost(&H->state_host, 4 * sizeof(int)));
+  CUDA_CHECK(cudaMallocHost(&H->state_host, dev::ST_COUNT * sizeof(int)));
+  CUDA_CHECK(cudaMallocHost(&H->host_S, dev::S_COUNT * sizeof(double)));
+  CUDA_CHECK(cudaMallocHost(&H->host_state, dev::ST_COUNT * sizeof(int)));
   CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
+// f, x: device pointers, or host pointers when `host` (copies inside the call)
 void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit, int* iters,
-                double* relres) {
+                double* relres, bool host = false) {
   MDD_REQUIRE(tol > 0 && maxit >= 0, 2, "tol must be > 0 and maxit >= 0");
   CUDA_CHECK(cudaSetDevice(H->device));
   cudaStream_t s = H->stream;
   const int n = H->n;
   using namespace dev;
-  H->launches = 0;
-  H->state.zero(s);
-  H->S.zero(s);
-  CUDA_CHECK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
-  CUDA_CHECK(cudaMemcpyAsync(H->r.p, f, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  H->dot(f, f, S_RR);
-  std::vector<double> hs(S_COUNT);
-  CUDA_CHECK(cudaMemcpyAsync(hs.data(), H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  double nf = std::sqrt(hs[S_RR]);
-  if (nf == 0.0) {
-    *iters = 0;
-    *relres = 0.0;
-    return;
-  }
-  hs[S_NF] = nf;
-  CUDA_CHECK(cudaMemcpyAsync(H->S.p + S_NF, &hs[S_NF], sizeof(double), cudaMemcpyHostToDevice, s));
-  cudaEvent_t* ev = H->ev;
+  // stage the solve: x = 0, r = f, S = {tol}, state = {maxit}
+  for (int k = 0; k < S_COUNT; ++k) H->host_S[k] = 0.0;
+  H->host_S[S_TOL] = tol;
+  for (int k = 0; k < ST_COUNT; ++k) H->host_state[k] = 0;
+  H->host_state[ST_MAXIT] = maxit;
+  CUDA_CHECK(cudaMemcpyAsync(H->S.p, H->host_S, S_COUNT * sizeof(double), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemcpyAsync(H->state.p, H->host_state, ST_COUNT * sizeof(int), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemsetAsync(H->x.p, 0, n * sizeof(double), s));
+  CUDA_CHECK(cudaMemcpyAsync(H->r.p, f, n * sizeof(double),
+                             host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
   const bool prof = H->profiling;
   for (auto& v : H->prof_ms) v = 0;
   for (auto& v : H->prof_launch) v = 0;
-  auto mark = [&](int k) { if (prof) CUDA_CHECK(cudaEventRecord(ev[k], s)); };
-  auto acc = [&](int phase, int a, int b) {
-    if (!prof) return;
-    float ms = 0;
-    CUDA_CHECK(cudaEventSynchronize(ev[b]));
-    CUDA_CHECK(cudaEventElapsedTime(&ms, ev[a], ev[b]));
-    H->prof_ms[phase] += ms;
-    H->prof_launch[phase] += 1;
-  };
-  mark(0);
-  H->apply_prec(H->r.p, H->z.p);
-  mark(1);
-  k_copy<<<nblk(n, 256), 256, 0, s>>>(n, H->z.p, H->p.p, H->state.p);
-  H->launches += 1;
-  H->dot(H->r.p, H->z.p, S_RZ);
-  int k = 0;
-  bool converged = false;
-  for (k = 1; k <= maxit; ++k) {
-    mark(2);
-    int blocks = nblk(n, 8);
-    k_spmv<<<blocks, 256, 0, s>>>(n, H->A_ptr.p, H->A_idx.p, H->A_val.p, H->p.p, H->q.p, H->p.p, H->part.p, H->state.p);
-    mark(3);
-    k_reduce<<<1, 256, 0, s>>>(blocks, H->part.p, H->S.p + S_PQ, H->state.p);
-    k_scalar_step<<<1, 1, 0, s>>>(0, H->S.p, H->state.p, tol, k);
-    k_update_xr<<<H->nparts, 256, 0, s>>>(n, x, H->r.p, H->p.p, H->q.p, H->S.p, H->part.p, H->state.p);
-    k_reduce<<<1, 256, 0, s>>>(H->nparts, H->part.p, H->S.p + S_RR, H->state.p);
-    k_scalar_step<<<1, 1, 0, s>>>(1, H->S.p, H->state.p, tol, k);
-    H->launches += 6;
-    mark(4);
-    CUDA_CHECK(cudaMemcpyAsync(H->state_host, H->state.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    acc(MDD_PROF_SPMV, 2, 3);
-    acc(MDD_PROF_VECTOR, 3, 4);
-    if (H->state_host[2]) throw Error(MDD_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0");
-    if (H->state_host[0]) { converged = true; break; }
-    mark(5);
-    H->apply_prec(H->r.p, H->z.p);
-    mark(6);
-    H->dot(H->r.p, H->z.p, S_RZNEW);
-    k_scalar_step<<<1, 1, 0, s>>>(2, H->S.p, H->state.p, tol, k);
-    k_update_p<<<H->nparts, 256, 0, s>>>(n, H->p.p, H->z.p, H->S.p, H->state.p);
-    H->launches += 2;
-    mark(7);
-    if (prof) {
-      acc(MDD_PROF_LOCAL_FWD, 5, 6);  // whole preconditioner (split below if needed)
-      acc(MDD_PROF_VECTOR, 6, 7);
+  if (!prof) {
+    // one graph launch runs the whole solve; the loop condition lives on the device
+    if (!H->graph_exec || H->graph_stream != s) H->build_graph();
+    CUDA_CHECK(cudaGraphLaunch(H->graph_exec, s));
+  } else {
+    // eager path with per-phase events (profiling only)
+    cudaEvent_t* ev = H->ev;
+    auto mark = [&](int k) { CUDA_CHECK(cudaEventRecord(ev[k], s)); };
+    auto acc = [&](int phase, int a, int b) {
+      float ms = 0;
+      CUDA_CHECK(cudaEventSynchronize(ev[b]));
+      CUDA_CHECK(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+      H->prof_ms[phase] += ms;
+      H->prof_launch[phase] += 1;
+    };
+    H->launches = 0;
+    H->enqueue_prologue();
+    for (int k = 1; k <= std::max(maxit, 1); ++k) {
+      H->enqueue_body(mark);
+      CUDA_CHECK(cudaMemcpyAsync(H->host_state, H->state.p, ST_COUNT * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      acc(MDD_PROF_SPMV, 2, 3);
+      acc(MDD_PROF_VECTOR, 3, 4);
+      acc(MDD_PROF_LOCAL_FWD, 4, 5);  // the whole preconditioner application
+      acc(MDD_PROF_VECTOR, 5, 6);
+      acc(MDD_PROF_TOTAL, 2, 6);
+      if (H->host_state[ST_STOP]) break;
     }
   }
-  CUDA_CHECK(cudaGetLastError());
-  CUDA_CHECK(cudaMemcpyAsync(hs.data(), H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(x, H->x.p, n * sizeof(double),
+                             host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  CUDA_CHECK(cudaMemcpyAsync(H->host_S, H->S.p, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaMemcpyAsync(H->host_state, H->state.p, ST_COUNT * sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  CUDA_CHECK(cudaGetLastError());
   H->check_aborts();
-  *iters = converged ? H->state_host[1] : maxit;
-  *relres = hs[S_REL];
-  if (!converged) throw Error(MDD_ERR_NOCONV, "PCG did not converge within maxit");
+  const int* st = H->host_state;
+  *iters = st[ST_ITERS];
+  *relres = H->host_S[S_REL];
+  if (!prof) H->launches = H->launches_prologue + H->launches_body * std::max(st[ST_ITERS], 1);
+  if (st[ST_BREAKDOWN]) throw Error(MDD_ERR_BREAKDOWN, "PCG breakdown: p^T A p <= 0");
+  if (!st[ST_CONVERGED]) throw Error(MDD_ERR_NOCONV, "PCG did not converge within maxit");
 }
 
 int guard(std::function<void()> f) {
@@ -842,24 +921,7 @@ int mdd_solve(mdd_handle h, const double* f, double* x, double tol, int maxit, i
 
 int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int maxit, int* iters, double* relres) {
   if (!h || !f || !x || !iters || !relres) { g_err = "null argument"; return MDD_ERR_ARG; }
-  return guard([&] {
-    CUDA_CHECK(cudaSetDevice(h->device));
-    DBuf<double> fd, xd;
-    fd.alloc(h->n);
-    xd.alloc(h->n);
-    CUDA_CHECK(cudaMemcpyAsync(fd.p, f, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
-    int rc = MDD_OK;
-    std::string msg;
-    try {
-      solve_impl(h, fd.p, xd.p, tol, maxit, iters, relres);
-    } catch (const Error& e) {
-      rc = e.code; msg = e.what();
-      if (rc != MDD_ERR_NOCONV) throw;
-    }
-    CUDA_CHECK(cudaMemcpyAsync(x, xd.p, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
-    if (rc != MDD_OK) throw Error(rc, msg);
-  });
+  return guard([&] { solve_impl(h, f, x, tol, maxit, iters, relres, true); });
 }
 
 int mdd_set_stream(mdd_handle h, void* stream) {
@@ -867,6 +929,7 @@ int mdd_set_stream(mdd_handle h, void* stream) {
   return guard([&] {
     CUDA_CHECK(cudaSetDevice(h->device));
     CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    h->drop_graph();
     if (h->own_stream) CUDA_CHECK(cudaStreamDestroy(h->stream));
     if (stream) {
       h->stream = (cudaStream_t)stream;

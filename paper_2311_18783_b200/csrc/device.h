@@ -78,7 +78,9 @@ struct DevFactor {
   // persistent sweep (sweep.cu)
   DBuf<int4> tasks;
   DBuf<int> nbf, nbb;
-  DBuf<unsigned long long> fwd_cnt, bwd_cnt, ctl;
+  DBuf<unsigned long long> fwd_cnt, bwd_cnt, ctl, stats;
+  std::string name;
+  ~DevFactor();
   int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, sweep_smem = 0, sweep_grid = 0;
   const int64_t* pro_ptr = nullptr;
   const int32_t* pro_pos = nullptr;
@@ -92,7 +94,10 @@ struct DevFactor {
   // -> source index) when gmap != NULL; with `out` the result is prolongated to
   // out[e] = sum of its copies (needs upload(prolong_n > 0)), else it stays in xb
   // (positions).
-  void sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s) const;
+  void sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s,
+             const int* stop = nullptr) const;
+  // accumulated device time (ns) and count of sweep launches (SW_TSUM / SW_TCNT)
+  void sweep_timing(unsigned long long* ns, unsigned long long* cnt, cudaStream_t s) const;
   // throws if a sweep aborted (spin timeout); resets the schedule state
   void check_abort(cudaStream_t s);
 };

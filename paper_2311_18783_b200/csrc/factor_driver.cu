@@ -1,6 +1,8 @@
 // Host drivers of the multifrontal factorisation and the level-scheduled
 // supernodal triangular solves (kernels in kernels.cu).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.h"
 
@@ -100,6 +102,31 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   ntasks = (int)tk.size();
   tasks.upload(tk);
+  if (getenv("MDD_SWEEP_STATS")) {
+    stats.alloc(8);
+    CUDA_CHECK(cudaMemset(stats.p, 0, 8 * sizeof(unsigned long long)));
+  }
+  if (getenv("MDD_PLAN_STATS")) {
+    fprintf(stderr, "[mdd plan %s] nsn %d levels %d entries %lld tasks %d (bwd %d)\n", name.c_str(), fp.nsn,
+            fp.nlevels, (long long)fp.factor_nnz(), ntasks, total_bwd);
+    for (int l = 0; l < fp.nlevels; ++l) {
+      long long ent = 0, emax = 0;
+      int ncmax = 0, nrmax = 0, tf = 0, tb = 0;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        const long long nc = fp.sn_ncol[g], no = fp.sn_noff[g];
+        const long long e = nc * (nc + 1) / 2 + nc * no;
+        ent += e;
+        emax = std::max(emax, e);
+        ncmax = std::max(ncmax, (int)nc);
+        nrmax = std::max(nrmax, (int)(nc + no));
+        tf += vf[g];
+        tb += vb[g];
+      }
+      fprintf(stderr, "  level %2d: sn %6d entries %10lld max %8lld ncmax %5d nrmax %5d fwd tasks %6d bwd tasks %6d\n",
+              l, fp.level_ptr[l + 1] - fp.level_ptr[l], ent, emax, ncmax, nrmax, tf, tb);
+    }
+  }
   nbf.upload(vf);
   nbb.upload(vb);
   fwd_cnt.alloc(std::max(fp.nsn, 1));
@@ -107,7 +134,11 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   ctl.alloc(dev::SW_COUNT);
   CUDA_CHECK(cudaMemset(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long)));
   CUDA_CHECK(cudaMemset(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long)));
-  CUDA_CHECK(cudaMemset(ctl.p, 0, ctl.n * sizeof(unsigned long long)));
+  {
+    std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
+    c0[dev::SW_T0] = ~0ull;
+    CUDA_CHECK(cudaMemcpy(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  }
   CUDA_CHECK(cudaDeviceSynchronize());
   sweep_smem = smem_d * (int)sizeof(double);
   MDD_REQUIRE(sweep_smem <= 200 * 1024, 5, "supernode too large for shared-memory staging");
@@ -121,7 +152,26 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   sweep_grid = nsm * per_sm;
 }
 
-void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s) const {
+DevFactor::~DevFactor() {
+  if (stats.p) {
+    unsigned long long v[8];
+    if (cudaMemcpy(v, stats.p, sizeof(v), cudaMemcpyDeviceToHost) == cudaSuccess)
+      fprintf(stderr, "[mdd sweep stats %s] cycles: fwd wait %llu work %llu | bwd wait %llu work %llu | "
+              "prolong wait %llu work %llu | ticket %llu | tasks %llu\n", name.c_str(), v[0], v[1], v[2],
+              v[3], v[4], v[5], v[6], v[7]);
+  }
+}
+
+void DevFactor::sweep_timing(unsigned long long* ns, unsigned long long* cnt, cudaStream_t s) const {
+  unsigned long long v[dev::SW_COUNT];
+  CUDA_CHECK(cudaMemcpyAsync(v, ctl.p, sizeof(v), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  *ns = v[dev::SW_TSUM];
+  *cnt = v[dev::SW_TCNT];
+}
+
+void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s,
+                      const int* stop) const {
   dev::SweepDev S;
   S.P = plan();
   S.L = L.p;
@@ -143,6 +193,8 @@ void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStr
   S.pro_ptr = pro_ptr;
   S.pro_pos = pro_pos;
   S.out = out;
+  S.stop = stop;
+  S.stats = stats.p;
   const int grid = std::max(1, std::min(sweep_grid, S.ntasks));
   dev::k_sweep<<<grid, dev::kSweepThreads, sweep_smem, s>>>(S);
 }
@@ -154,7 +206,9 @@ void DevFactor::check_abort(cudaStream_t s) {
   if (ab) {
     CUDA_CHECK(cudaMemsetAsync(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long), s));
     CUDA_CHECK(cudaMemsetAsync(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long), s));
-    CUDA_CHECK(cudaMemsetAsync(ctl.p, 0, ctl.n * sizeof(unsigned long long), s));
+    std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
+    c0[dev::SW_T0] = ~0ull;
+    CUDA_CHECK(cudaMemcpyAsync(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
     throw Error(5, "supernodal sweep aborted (dependency wait timed out)");
   }

@@ -330,25 +330,39 @@ __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __
   if (threadIdx.x == 0) *out = tmp[0];
 }
 
-// scalar recurrences of PCG (single thread)
-__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state, double tol,
-                              int iter) {
-  if (state[0]) return;
+// scalar recurrences of PCG (single thread).  state[ST_STOP] makes every later
+// kernel of the iteration a no-op; state[ST_ITERS] counts iterations on the device
+__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state) {
+  if (state[ST_STOP]) return;
   switch (op) {
     case 0:  // after q = A p:  alpha = rz / pq
-      if (!(S[S_PQ] > 0.0)) { state[2] = 1; state[0] = 1; return; }
+      if (!(S[S_PQ] > 0.0)) { state[ST_BREAKDOWN] = 1; state[ST_STOP] = 1; return; }
       S[S_ALPHA] = S[S_RZ] / S[S_PQ];
       break;
-    case 1:  // after r update: convergence
+    case 1: {  // after the r update: convergence / iteration limit
+      const int it = state[ST_ITERS] + 1;
+      state[ST_ITERS] = it;
       S[S_REL] = sqrt(S[S_RR]) / S[S_NF];
-      state[1] = iter;
-      if (S[S_REL] <= tol) state[0] = 1;
+      if (S[S_REL] <= S[S_TOL]) { state[ST_CONVERGED] = 1; state[ST_STOP] = 1; }
+      else if (it >= state[ST_MAXIT]) state[ST_STOP] = 1;
       break;
+    }
     case 2:  // after z = M r: beta
       S[S_BETA] = S[S_RZNEW] / S[S_RZ];
       S[S_RZ] = S[S_RZNEW];
       break;
+    case 3:  // prologue: ||f||; f = 0 -> x = 0 converged in 0 iterations
+      S[S_NF] = sqrt(S[S_RR]);
+      S[S_REL] = S[S_NF] > 0.0 ? 1.0 : 0.0;
+      if (!(S[S_NF] > 0.0)) { state[ST_CONVERGED] = 1; state[ST_STOP] = 1; }
+      else if (state[ST_MAXIT] <= 0) state[ST_STOP] = 1;
+      break;
   }
+}
+
+// device-side loop condition of the CUDA-graph WHILE node
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ state) {
+  cudaGraphSetConditional(h, state[ST_STOP] ? 0u : 1u);
 }
 
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,

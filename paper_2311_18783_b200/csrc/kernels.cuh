@@ -90,7 +90,7 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
 
 // -------------------------------------------- supernodal triangular sweeps
 // (sweep.cu) control words of a persistent sweep
-enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_COUNT };
+enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 constexpr int kSweepThreads = 256;
 
 struct SweepDev {
@@ -114,6 +114,8 @@ struct SweepDev {
   const int64_t* pro_ptr;        // prolongation (global dof -> positions)
   const int32_t* pro_pos;
   double* out;                   // prolongation target (global)
+  const int* stop;               // PCG stop flag (nullable): set -> no-op launch
+  unsigned long long* stats;     // optional cycle accounting (MDD_SWEEP_STATS=1)
 };
 __global__ void k_sweep(SweepDev S);
 
@@ -130,8 +132,8 @@ __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __
                            double* __restrict__ part, const int* __restrict__ stop);
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
                          const int* __restrict__ stop);
-__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state,
-                              double tol, int iter);
+__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state);
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ state);
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
                             const double* __restrict__ p, const double* __restrict__ q,
                             const double* __restrict__ S, double* __restrict__ part,
@@ -154,7 +156,8 @@ __global__ void k_csr_warp_spmv(int nrows, const int64_t* __restrict__ ptr,
                                 const int* __restrict__ stop);
 
 // scalar slots of the PCG state
-enum { S_RZ = 0, S_PQ, S_ALPHA, S_RR, S_NF, S_BETA, S_RZNEW, S_REL, S_TMP, S_COUNT };
-// state[0] = stop flag, state[1] = iterations done, state[2] = breakdown
+enum { S_RZ = 0, S_PQ, S_ALPHA, S_RR, S_NF, S_BETA, S_RZNEW, S_REL, S_TOL, S_TMP, S_COUNT };
+// device state words of a solve
+enum { ST_STOP = 0, ST_ITERS, ST_BREAKDOWN, ST_MAXIT, ST_CONVERGED, ST_COUNT };
 }  // namespace dev
 }  // namespace mdd

@@ -75,15 +75,24 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
   const PlanDev& P = S.P;
+  if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
+  if (tid == 0) atomicMin(&S.ctl[SW_T0], globaltimer());
+  // optional per-CTA cycle accounting (S.stats != NULL): [type*2] wait, [type*2+1] work,
+  // [6] ticket, [7] tasks
+  long long st_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long c_prev = clock64();
 
   for (;;) {
     if (tid == 0) s_task = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
     __syncthreads();
     const int t = s_task;
+    if (S.stats && tid == 0) { long long c = clock64(); st_acc[6] += c - c_prev; c_prev = c; }
     if (t >= S.ntasks) break;
     const int4 tk = S.tasks[t];
     const int type = tk.x, g = tk.y, lo = tk.z, hi = tk.w;
+#define STAT_MARK(slot) \
+  if (S.stats && tid == 0) { long long c = clock64(); st_acc[(slot)] += c - c_prev; c_prev = c; }
 
     if (type == 0) {
       // ------------------------------------------------ forward row block
@@ -97,6 +106,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
         s_ok = ok;
       }
       __syncthreads();
+      STAT_MARK(0);
       if (s_ok) {
         const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
         const i64 col0 = P.sn_col0[g];
@@ -173,6 +183,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
         __syncthreads();
         if (tid == 0) signal_add(&S.fwd_cnt[g]);
       }
+      STAT_MARK(1);
     } else if (type == 1) {
       // ------------------------------------------------ backward column block
       if (tid == 0) {
@@ -184,6 +195,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
         s_ok = ok;
       }
       __syncthreads();
+      STAT_MARK(2);
       if (s_ok) {
         const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
         const i64 col0 = P.sn_col0[g];
@@ -228,6 +240,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
           atomicAdd(&S.ctl[SW_BWD_DONE], 1ull);
         }
       }
+      STAT_MARK(3);
     } else {
       // ------------------------------------------------ prolongation chunk
       if (tid == 0) {
@@ -237,6 +250,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
         s_ok = ok;
       }
       __syncthreads();
+      STAT_MARK(4);
       if (s_ok) {
         for (int e = lo + tid; e < hi; e += nt) {
           double s = 0.0;
@@ -244,14 +258,24 @@ __global__ void __launch_bounds__(kSweepThreads) k_sweep(SweepDev S) {
           S.out[e] = s;
         }
       }
+      __syncthreads();
+      STAT_MARK(5);
     }
+    if (S.stats && tid == 0) st_acc[7] += 1;
     __syncthreads();
   }
+#undef STAT_MARK
+  if (S.stats && tid == 0)
+    for (int q = 0; q < 8; ++q) atomicAdd(&S.stats[q], (unsigned long long)st_acc[q]);
   // exit protocol: the last CTA resets the ticket and advances the epoch
   if (tid == 0) {
     __threadfence();
     const unsigned long long prev = atomicAdd(&S.ctl[SW_EXIT], 1ull);
     if (prev == (unsigned long long)gridDim.x - 1) {
+      // device-side duration of this launch (first CTA start -> last CTA exit)
+      S.ctl[SW_TSUM] += globaltimer() - S.ctl[SW_T0];
+      S.ctl[SW_TCNT] += 1;
+      S.ctl[SW_T0] = ~0ull;
       S.ctl[SW_TICKET] = 0;
       S.ctl[SW_EXIT] = 0;
       S.ctl[SW_EPOCH] = cur;
