@@ -75,20 +75,27 @@ struct DevFactor {
   DBuf<int64_t> col0, rowptr, offrows, lptr, uptr, fptr, umptr, child_ptr, asm_ptr, asm_src;
   DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn, parent;
   DBuf<double> L, dinv, upd, xf, xb;
-  // persistent sweep (sweep.cu)
-  DBuf<int4> tasks;
-  DBuf<int> nbf, nbb;
-  DBuf<unsigned long long> fwd_cnt, bwd_cnt, ctl, stats;
-  std::string name;
-  ~DevFactor();
-  int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, sweep_smem = 0, sweep_grid = 0;
+  // persistent sweep (sweep.cu): tiles and schedule
+  DBuf<int4> tasks, tiles;
+  DBuf<int64_t> tile_off, sn_fpart, sn_bpart, sn_tg;
+  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc;
+  DBuf<double> Lt, fpart, bpart, tg;
+  DBuf<unsigned long long> fwd_cnt, bwd_cnt, rb_cnt, cb_cnt, asm_cnt, ctl, stats;
+  int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, ntiles = 0, sweep_grid = 0;
+  int64_t lt_size = 0;
   const int64_t* pro_ptr = nullptr;
   const int32_t* pro_pos = nullptr;
+  std::string name;
+  DevFactor() = default;
+  DevFactor(const DevFactor&) = delete;
+  ~DevFactor();
   dev::PlanDev plan() const;
+  dev::SweepDev sweep_dev() const;
   // prolong_n > 0 appends prolongation chunks over prolong_n global dofs
   void upload(int prolong_n = 0, const int64_t* pro_ptr_dev = nullptr,
               const int32_t* pro_pos_dev = nullptr);
-  // numeric multifrontal factorisation from a device value array `src`
+  // numeric multifrontal factorisation from a device value array `src`; the
+  // panels are then re-laid out into the sweep tiles
   int factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
   // x = A^{-1} b in one persistent launch.  b is gathered through gmap (positions
   // -> source index) when gmap != NULL; with `out` the result is prolongated to
@@ -100,6 +107,7 @@ struct DevFactor {
   void sweep_timing(unsigned long long* ns, unsigned long long* cnt, cudaStream_t s) const;
   // throws if a sweep aborted (spin timeout); resets the schedule state
   void check_abort(cudaStream_t s);
+  void reset_counters(cudaStream_t s);
 };
 
 }  // namespace mdd

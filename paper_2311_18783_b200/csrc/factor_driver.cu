@@ -30,9 +30,6 @@ dev::PlanDev DevFactor::plan() const {
 }
 
 namespace {
-// tasks of roughly kTaskEntries panel entries (~192 KB) so top-of-tree supernodes
-// spread over several SMs while leaves stay one task each
-constexpr int64_t kTaskEntries = 32768;
 constexpr int kProlongChunk = 2048;
 }  // namespace
 
@@ -59,39 +56,62 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   upd.alloc(std::max<int64_t>(fp.usize, 1));
   xf.alloc(std::max<int64_t>(fp.ntot, 1));
   xb.alloc(std::max<int64_t>(fp.ntot, 1));
-  // ---- sweep schedule
+  // ---- tile geometry per supernode
+  const int nsn = fp.nsn;
+  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn), vncb(nsn), vrbc(nsn), vcbc(nsn);
+  std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0), vtg(nsn, 0);
+  std::vector<std::vector<int>> sn_tiles(nsn);
+  std::vector<int4> tl;
+  std::vector<int64_t> toff;
+  int64_t off = 0, nfp = 0, nbp = 0, ntg = 0;
+  int nrbc = 0, ncbc = 0;
+  for (int g = 0; g < nsn; ++g) {
+    const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
+    int RB, CB;
+    if (nr <= dev::kVecMax && (int64_t)nr * nc <= dev::kTileMax) {
+      RB = nr;
+      CB = nc;
+    } else {
+      CB = std::min(nc, 64);
+      RB = std::min(dev::kVecMax, std::max(32, (dev::kTileMax / CB) / 32 * 32));
+    }
+    const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
+    vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
+    if (nrb * ncb > 1) {
+      vfp[g] = nfp; nfp += (int64_t)ncb * nr;
+      vbp[g] = nbp; nbp += (int64_t)nrb * nc;
+      vtg[g] = ntg; ntg += nr;
+      vrbc[g] = nrbc; nrbc += nrb;
+      vcbc[g] = ncbc; ncbc += ncb;
+    }
+    for (int rb = 0; rb < nrb; ++rb) {
+      const int rend = std::min(nr, (rb + 1) * RB), rows = rend - rb * RB;
+      for (int cb = 0; cb < ncb && cb * CB < rend; ++cb) {
+        const int cols = std::min(CB, nc - cb * CB);
+        sn_tiles[g].push_back((int)tl.size());
+        tl.push_back(make_int4(g, rb, cb, 0));
+        toff.push_back(off);
+        off += ((int64_t)rows * cols + 1) & ~1LL;  // 16-byte aligned tiles
+      }
+    }
+  }
+  ntiles = (int)tl.size();
+  lt_size = off;
+  // ---- schedule: forward (level order; assemble task before the tiles of a big
+  // supernode), backward (reverse level order), prolongation
   std::vector<int4> tk;
-  std::vector<int> vf(fp.nsn), vb(fp.nsn);
-  int smem_d = 1;
   for (int l = 0; l < fp.nlevels; ++l)
     for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
       const int g = fp.level_sn[k];
-      const int nc = fp.sn_ncol[g], no = fp.sn_noff[g], nr = nc + no;
-      const int64_t ent = (int64_t)nc * (nc + 1) / 2 + (int64_t)nc * no;
-      int rb = nr;
-      if (nr > dev::kSweepThreads || ent > kTaskEntries) {
-        rb = (int)std::min<int64_t>(dev::kSweepThreads, std::max<int64_t>(32, kTaskEntries / nc));
-        rb = rb / 32 * 32;
-      }
-      int cnt = 0;
-      for (int r0 = 0; r0 < nr; r0 += rb, ++cnt) tk.push_back(make_int4(0, g, r0, std::min(nr, r0 + rb)));
-      vf[g] = cnt;
-      smem_d = std::max(smem_d, nc + std::min(nr, rb) + dev::kSweepThreads);
+      if (vnrb[g] * vncb[g] > 1) tk.push_back(make_int4(3, g, 0, 0));
+      for (int t : sn_tiles[g]) tk.push_back(make_int4(0, t, 0, 0));
     }
-  ntasks_noprolong = 0;
   total_bwd = 0;
   for (int l = fp.nlevels - 1; l >= 0; --l)
     for (int k = fp.level_ptr[l + 1] - 1; k >= fp.level_ptr[l]; --k) {
       const int g = fp.level_sn[k];
-      const int nc = fp.sn_ncol[g], no = fp.sn_noff[g], nr = nc + no;
-      const int64_t ent = (int64_t)nc * (nc + 1) / 2 + (int64_t)nc * no;
-      int cb = nc;
-      if (ent > kTaskEntries) cb = (int)std::max<int64_t>(16, kTaskEntries / nr / 16 * 16);
-      int cnt = 0;
-      for (int c0 = 0; c0 < nc; c0 += cb, ++cnt) tk.push_back(make_int4(1, g, c0, std::min(nc, c0 + cb)));
-      vb[g] = cnt;
-      total_bwd += cnt;
-      smem_d = std::max(smem_d, nr + (dev::kSweepThreads / 32) * 16);
+      for (int t : sn_tiles[g]) tk.push_back(make_int4(1, t, 0, 0));
+      total_bwd += vncb[g];
     }
   ntasks_noprolong = (int)tk.size();
   if (prolong_n > 0) {
@@ -102,16 +122,35 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   ntasks = (int)tk.size();
   tasks.upload(tk);
+  tiles.upload(tl);
+  tile_off.upload(toff);
+  sn_RB.upload(vRB); sn_CB.upload(vCB); sn_nrb.upload(vnrb); sn_ncb.upload(vncb);
+  sn_rbc.upload(vrbc); sn_cbc.upload(vcbc);
+  sn_fpart.upload(vfp); sn_bpart.upload(vbp); sn_tg.upload(vtg);
+  fpart.alloc(std::max<int64_t>(nfp, 1));
+  bpart.alloc(std::max<int64_t>(nbp, 1));
+  tg.alloc(std::max<int64_t>(ntg, 1));
+  rb_cnt.alloc(std::max(nrbc, 1));
+  cb_cnt.alloc(std::max(ncbc, 1));
+  asm_cnt.alloc(std::max(nsn, 1));
+  fwd_cnt.alloc(std::max(nsn, 1));
+  bwd_cnt.alloc(std::max(nsn, 1));
+  ctl.alloc(dev::SW_COUNT);
+  reset_counters(nullptr);
+  CUDA_CHECK(cudaDeviceSynchronize());
   if (getenv("MDD_SWEEP_STATS")) {
-    stats.alloc(8);
-    CUDA_CHECK(cudaMemset(stats.p, 0, 8 * sizeof(unsigned long long)));
+    stats.alloc(10);
+    CUDA_CHECK(cudaMemset(stats.p, 0, 10 * sizeof(unsigned long long)));
   }
   if (getenv("MDD_PLAN_STATS")) {
-    fprintf(stderr, "[mdd plan %s] nsn %d levels %d entries %lld tasks %d (bwd %d)\n", name.c_str(), fp.nsn,
-            fp.nlevels, (long long)fp.factor_nnz(), ntasks, total_bwd);
+    int nbig = 0;
+    for (int g = 0; g < nsn; ++g) nbig += vnrb[g] * vncb[g] > 1;
+    fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) tasks %d\n",
+            name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(), ntiles,
+            100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), ntasks);
     for (int l = 0; l < fp.nlevels; ++l) {
       long long ent = 0, emax = 0;
-      int ncmax = 0, nrmax = 0, tf = 0, tb = 0;
+      int ncmax = 0, nrmax = 0, tcount = 0, big = 0;
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         const long long nc = fp.sn_ncol[g], no = fp.sn_noff[g];
@@ -120,45 +159,71 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         emax = std::max(emax, e);
         ncmax = std::max(ncmax, (int)nc);
         nrmax = std::max(nrmax, (int)(nc + no));
-        tf += vf[g];
-        tb += vb[g];
+        tcount += (int)sn_tiles[g].size();
+        big += vnrb[g] * vncb[g] > 1;
       }
-      fprintf(stderr, "  level %2d: sn %6d entries %10lld max %8lld ncmax %5d nrmax %5d fwd tasks %6d bwd tasks %6d\n",
-              l, fp.level_ptr[l + 1] - fp.level_ptr[l], ent, emax, ncmax, nrmax, tf, tb);
+      fprintf(stderr, "  level %2d: sn %6d (big %4d) entries %10lld max %8lld ncmax %5d nrmax %5d tiles %6d\n", l,
+              fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, emax, ncmax, nrmax, tcount);
     }
   }
-  nbf.upload(vf);
-  nbb.upload(vb);
-  fwd_cnt.alloc(std::max(fp.nsn, 1));
-  bwd_cnt.alloc(std::max(fp.nsn, 1));
-  ctl.alloc(dev::SW_COUNT);
-  CUDA_CHECK(cudaMemset(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long)));
-  CUDA_CHECK(cudaMemset(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long)));
-  {
-    std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
-    c0[dev::SW_T0] = ~0ull;
-    CUDA_CHECK(cudaMemcpy(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
-  }
-  CUDA_CHECK(cudaDeviceSynchronize());
-  sweep_smem = smem_d * (int)sizeof(double);
-  MDD_REQUIRE(sweep_smem <= 200 * 1024, 5, "supernode too large for shared-memory staging");
-  if (sweep_smem > 48 * 1024)
-    CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, sweep_smem));
+  const int smem = dev::kSweepSmemDoubles * (int)sizeof(double);
+  CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int dev_id = 0, nsm = 0, per_sm = 0;
   CUDA_CHECK(cudaGetDevice(&dev_id));
   CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, sweep_smem));
+  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
   MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
   sweep_grid = nsm * per_sm;
 }
 
+void DevFactor::reset_counters(cudaStream_t s) {
+  for (DBuf<unsigned long long>* c : {&fwd_cnt, &bwd_cnt, &rb_cnt, &cb_cnt, &asm_cnt})
+    CUDA_CHECK(cudaMemsetAsync(c->p, 0, c->n * sizeof(unsigned long long), s));
+  std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
+  c0[dev::SW_T0] = ~0ull;
+  CUDA_CHECK(cudaMemcpyAsync(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+dev::SweepDev DevFactor::sweep_dev() const {
+  dev::SweepDev S;
+  S.P = plan();
+  S.dinv = dinv.p;
+  S.tasks = tasks.p;
+  S.ntasks = ntasks;
+  S.total_bwd = total_bwd;
+  S.parent = parent.p;
+  S.tiles = tiles.p;
+  S.tile_off = tile_off.p;
+  S.Lt = Lt.p;
+  S.sn_RB = sn_RB.p; S.sn_CB = sn_CB.p; S.sn_nrb = sn_nrb.p; S.sn_ncb = sn_ncb.p;
+  S.sn_fpart = sn_fpart.p; S.sn_bpart = sn_bpart.p; S.sn_tg = sn_tg.p;
+  S.sn_rbc = sn_rbc.p; S.sn_cbc = sn_cbc.p;
+  S.fpart = fpart.p; S.bpart = bpart.p; S.tg = tg.p;
+  S.rb_cnt = rb_cnt.p; S.cb_cnt = cb_cnt.p; S.asm_cnt = asm_cnt.p;
+  S.fwd_cnt = fwd_cnt.p;
+  S.bwd_cnt = bwd_cnt.p;
+  S.ctl = ctl.p;
+  S.upd = upd.p;
+  S.xf = xf.p;
+  S.xb = xb.p;
+  S.b = nullptr;
+  S.gmap = nullptr;
+  S.pro_ptr = pro_ptr;
+  S.pro_pos = pro_pos;
+  S.out = nullptr;
+  S.stop = nullptr;
+  S.stats = stats.p;
+  return S;
+}
+
 DevFactor::~DevFactor() {
   if (stats.p) {
-    unsigned long long v[8];
+    unsigned long long v[10];
     if (cudaMemcpy(v, stats.p, sizeof(v), cudaMemcpyDeviceToHost) == cudaSuccess)
       fprintf(stderr, "[mdd sweep stats %s] cycles: fwd wait %llu work %llu | bwd wait %llu work %llu | "
-              "prolong wait %llu work %llu | ticket %llu | tasks %llu\n", name.c_str(), v[0], v[1], v[2],
-              v[3], v[4], v[5], v[6], v[7]);
+              "prolong wait %llu work %llu | assemble wait %llu work %llu | ticket %llu | tasks %llu\n",
+              name.c_str(), v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
   }
 }
 
@@ -172,31 +237,14 @@ void DevFactor::sweep_timing(unsigned long long* ns, unsigned long long* cnt, cu
 
 void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s,
                       const int* stop) const {
-  dev::SweepDev S;
-  S.P = plan();
-  S.L = L.p;
-  S.dinv = dinv.p;
-  S.tasks = tasks.p;
+  dev::SweepDev S = sweep_dev();
   S.ntasks = out ? ntasks : ntasks_noprolong;
-  S.total_bwd = total_bwd;
-  S.nbf = nbf.p;
-  S.nbb = nbb.p;
-  S.parent = parent.p;
-  S.fwd_cnt = fwd_cnt.p;
-  S.bwd_cnt = bwd_cnt.p;
-  S.ctl = ctl.p;
-  S.upd = upd.p;
-  S.xf = xf.p;
-  S.xb = xb.p;
   S.b = b;
   S.gmap = gmap;
-  S.pro_ptr = pro_ptr;
-  S.pro_pos = pro_pos;
   S.out = out;
   S.stop = stop;
-  S.stats = stats.p;
   const int grid = std::max(1, std::min(sweep_grid, S.ntasks));
-  dev::k_sweep<<<grid, dev::kSweepThreads, sweep_smem, s>>>(S);
+  dev::k_sweep<<<grid, dev::kSweepThreads, dev::kSweepSmemDoubles * sizeof(double), s>>>(S);
 }
 
 void DevFactor::check_abort(cudaStream_t s) {
@@ -204,12 +252,7 @@ void DevFactor::check_abort(cudaStream_t s) {
   CUDA_CHECK(cudaMemcpyAsync(&ab, ctl.p + dev::SW_ABORT, sizeof(ab), cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   if (ab) {
-    CUDA_CHECK(cudaMemsetAsync(fwd_cnt.p, 0, fwd_cnt.n * sizeof(unsigned long long), s));
-    CUDA_CHECK(cudaMemsetAsync(bwd_cnt.p, 0, bwd_cnt.n * sizeof(unsigned long long), s));
-    std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
-    c0[dev::SW_T0] = ~0ull;
-    CUDA_CHECK(cudaMemcpyAsync(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
+    reset_counters(s);
     throw Error(5, "supernodal sweep aborted (dependency wait timed out)");
   }
 }
@@ -232,9 +275,16 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
   CUDA_CHECK(cudaStreamSynchronize(s));
   int e = 0;
   CUDA_CHECK(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
-  if (mode == 2) return e;
-  MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");
-  return 0;
+  if (mode != 2) MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");
+  // P-form panels -> contiguous sweep tiles; the column-major panels are dropped
+  Lt.alloc(std::max<int64_t>(lt_size, 2));
+  if (ntiles > 0) {
+    dev::k_tile_relayout<<<ntiles, 256, 0, s>>>(sweep_dev(), ntiles, L.p, lptr.p);
+    CUDA_CHECK(cudaGetLastError());
+  }
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  L.release();
+  return mode == 2 ? e : 0;
 }
 
 }  // namespace mdd

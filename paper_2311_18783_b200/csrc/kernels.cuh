@@ -92,19 +92,38 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
 // (sweep.cu) control words of a persistent sweep
 enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 constexpr int kSweepThreads = 256;
+constexpr int kTileMax = 4096;   // doubles per tile (32 KB, one TMA bulk copy)
+constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
+constexpr int kSweepSmemDoubles = 2 * kTileMax + 2 * kVecMax + kSweepThreads;
 
 struct SweepDev {
   PlanDev P;
-  const double* L;               // P-form panels
   const double* dinv;
-  const int4* tasks;             // {type 0 fwd / 1 bwd / 2 prolong, supernode, lo, hi}
+  const int4* tasks;             // {type 0 fwd tile / 1 bwd tile / 2 prolong / 3 assemble, idx, lo, hi}
   int ntasks;
-  int total_bwd;                 // bwd tasks per launch
-  const int* nbf;                // fwd tasks per supernode
-  const int* nbb;                // bwd tasks per supernode
+  int total_bwd;                 // backward column blocks per launch
   const int* parent;             // supernode parent (-1 root)
-  unsigned long long* fwd_cnt;   // cumulative completion counters
-  unsigned long long* bwd_cnt;
+  // tiles
+  const int4* tiles;             // {supernode, row block, column block, 0}
+  const int64_t* tile_off;       // into Lt
+  const double* Lt;              // tiled P-form panels
+  const int* sn_RB;              // tile rows / columns / counts per supernode
+  const int* sn_CB;
+  const int* sn_nrb;
+  const int* sn_ncb;
+  const int64_t* sn_fpart;       // big supernodes: partial sums / rhs offsets
+  const int64_t* sn_bpart;
+  const int64_t* sn_tg;
+  const int* sn_rbc;             // offsets of the row-block / column-block counters
+  const int* sn_cbc;
+  double* fpart;
+  double* bpart;
+  double* tg;
+  unsigned long long* rb_cnt;
+  unsigned long long* cb_cnt;
+  unsigned long long* asm_cnt;
+  unsigned long long* fwd_cnt;   // row blocks finished (cumulative)
+  unsigned long long* bwd_cnt;   // column blocks finished (cumulative)
   unsigned long long* ctl;       // SW_* words
   double* upd;                   // update vectors (noff per supernode)
   double* xf;                    // forward result z (positions)
@@ -118,6 +137,9 @@ struct SweepDev {
   unsigned long long* stats;     // optional cycle accounting (MDD_SWEEP_STATS=1)
 };
 __global__ void k_sweep(SweepDev S);
+__global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,
+                                const int64_t* __restrict__ lptr);
+
 
 // prolongation sum_i R_i^T x_i: out[e] = sum over the copies of dof e (fixed order)
 __global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
