@@ -56,10 +56,13 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   upd.alloc(std::max<int64_t>(fp.usize, 1));
   xf.alloc(std::max<int64_t>(fp.ntot, 1));
   xb.alloc(std::max<int64_t>(fp.ntot, 1));
-  // ---- tile geometry per supernode
+  // ---- tile geometry per supernode.  "single": swept by one CTA (column tiles
+  // over all nr rows, accumulated in shared memory); "big": RB x CB tiles spread
+  // over CTAs with partial sums
   const int nsn = fp.nsn;
-  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn), vncb(nsn), vrbc(nsn), vcbc(nsn);
-  std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0), vtg(nsn, 0);
+  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn), vncb(nsn), vrbc(nsn, 0), vcbc(nsn, 0);
+  std::vector<uint8_t> single(nsn);
+  std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0), vtg(nsn, 0), stored(nsn);
   std::vector<std::vector<int>> sn_tiles(nsn);
   std::vector<int4> tl;
   std::vector<int64_t> toff;
@@ -67,17 +70,19 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   int nrbc = 0, ncbc = 0;
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
+    stored[g] = (int64_t)nr * nc;
+    single[g] = nr <= dev::kVecMax && stored[g] <= dev::kSingleMax;
     int RB, CB;
-    if (nr <= dev::kVecMax && (int64_t)nr * nc <= dev::kTileMax) {
+    if (single[g]) {
       RB = nr;
-      CB = nc;
+      CB = std::max(1, std::min(nc, dev::kTileMax / nr));
     } else {
       CB = std::min(nc, 64);
       RB = std::min(dev::kVecMax, std::max(32, (dev::kTileMax / CB) / 32 * 32));
     }
     const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
     vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
-    if (nrb * ncb > 1) {
+    if (!single[g]) {
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;
       vbp[g] = nbp; nbp += (int64_t)nrb * nc;
       vtg[g] = ntg; ntg += nr;
@@ -97,31 +102,93 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   ntiles = (int)tl.size();
   lt_size = off;
-  // ---- schedule: forward (level order; assemble task before the tiles of a big
-  // supernode), backward (reverse level order), prolongation
+  // ---- clusters: a single-only subtree of <= kClusterMax stored entries is one
+  // task (postorder); a single supernode above such subtrees is its own cluster
+  std::vector<std::vector<int>> kids(nsn);
+  for (int g = 0; g < nsn; ++g)
+    if (fp.sn_parent[g] >= 0) kids[fp.sn_parent[g]].push_back(g);
+  std::vector<uint8_t> sub_ok(nsn);
+  std::vector<int64_t> sub_sz(nsn);
+  for (int g = 0; g < nsn; ++g) {  // children precede parents
+    bool okg = single[g];
+    int64_t sz = stored[g];
+    for (int c : kids[g]) { okg = okg && sub_ok[c]; sz += sub_sz[c]; }
+    sub_ok[g] = okg;
+    sub_sz[g] = sz;
+  }
+  struct Cl { int root; int wait; std::vector<int> members; };
+  std::vector<Cl> clusters;
+  std::vector<int> bigs;
+  std::vector<int> stack;
+  for (int g = 0; g < nsn; ++g)
+    if (fp.sn_parent[g] < 0) stack.push_back(g);
+  while (!stack.empty()) {
+    const int g = stack.back();
+    stack.pop_back();
+    if (single[g] && sub_ok[g] && sub_sz[g] <= dev::kClusterMax) {
+      Cl c{g, 0, {}};
+      std::vector<int> st{g}, order;
+      while (!st.empty()) {  // preorder, reversed below into a postorder
+        const int v = st.back();
+        st.pop_back();
+        order.push_back(v);
+        for (int k : kids[v]) st.push_back(k);
+      }
+      c.members.assign(order.rbegin(), order.rend());
+      clusters.push_back(std::move(c));
+      continue;
+    }
+    if (single[g]) clusters.push_back(Cl{g, kids[g].empty() ? 0 : 1, {g}});
+    else bigs.push_back(g);
+    for (int k : kids[g]) stack.push_back(k);
+  }
+  // ---- schedule: forward work by level of its top supernode, backward work in
+  // the reverse order, prolongation last.  Every wait targets an earlier ticket.
+  std::vector<std::vector<int>> cl_at(fp.nlevels), big_at(fp.nlevels);
+  for (int c = 0; c < (int)clusters.size(); ++c) cl_at[fp.sn_level[clusters[c].root]].push_back(c);
+  for (int g : bigs) big_at[fp.sn_level[g]].push_back(g);
   std::vector<int4> tk;
-  for (int l = 0; l < fp.nlevels; ++l)
-    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-      const int g = fp.level_sn[k];
-      if (vnrb[g] * vncb[g] > 1) tk.push_back(make_int4(3, g, 0, 0));
-      for (int t : sn_tiles[g]) tk.push_back(make_int4(0, t, 0, 0));
+  std::vector<int> ttp(1, 0), ttl;
+  auto add_task = [&](int4 t, const std::vector<int>& tiles_) {
+    tk.push_back(t);
+    ttl.insert(ttl.end(), tiles_.begin(), tiles_.end());
+    ttp.push_back((int)ttl.size());
+  };
+  const std::vector<int> none;
+  for (int l = 0; l < fp.nlevels; ++l) {
+    for (int c : cl_at[l]) {
+      std::vector<int> ts;
+      for (int g : clusters[c].members) ts.insert(ts.end(), sn_tiles[g].begin(), sn_tiles[g].end());
+      add_task(make_int4(4, clusters[c].root, clusters[c].wait, 0), ts);
     }
+    for (int g : big_at[l]) {
+      add_task(make_int4(3, g, 0, 0), none);
+      for (int t : sn_tiles[g]) add_task(make_int4(0, t, 0, 0), std::vector<int>{t});
+    }
+  }
   total_bwd = 0;
-  for (int l = fp.nlevels - 1; l >= 0; --l)
-    for (int k = fp.level_ptr[l + 1] - 1; k >= fp.level_ptr[l]; --k) {
-      const int g = fp.level_sn[k];
-      for (int t : sn_tiles[g]) tk.push_back(make_int4(1, t, 0, 0));
-      total_bwd += vncb[g];
+  for (int g = 0; g < nsn; ++g) total_bwd += vncb[g];
+  for (int l = fp.nlevels - 1; l >= 0; --l) {
+    for (int g : big_at[l])
+      for (int t : sn_tiles[g]) add_task(make_int4(1, t, 0, 0), std::vector<int>{t});
+    for (int c : cl_at[l]) {
+      std::vector<int> ts;
+      for (auto it2 = clusters[c].members.rbegin(); it2 != clusters[c].members.rend(); ++it2)
+        ts.insert(ts.end(), sn_tiles[*it2].begin(), sn_tiles[*it2].end());
+      add_task(make_int4(5, clusters[c].root, 0, 0), ts);
     }
+  }
   ntasks_noprolong = (int)tk.size();
   if (prolong_n > 0) {
     for (int e0 = 0; e0 < prolong_n; e0 += kProlongChunk)
-      tk.push_back(make_int4(2, 0, e0, std::min(prolong_n, e0 + kProlongChunk)));
+      add_task(make_int4(2, 0, e0, std::min(prolong_n, e0 + kProlongChunk)), none);
     pro_ptr = pro_ptr_dev;
     pro_pos = pro_pos_dev;
   }
   ntasks = (int)tk.size();
   tasks.upload(tk);
+  tt_ptr.upload(ttp);
+  task_tiles.upload(ttl);
   tiles.upload(tl);
   tile_off.upload(toff);
   sn_RB.upload(vRB); sn_CB.upload(vCB); sn_nrb.upload(vnrb); sn_ncb.upload(vncb);
@@ -144,10 +211,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   if (getenv("MDD_PLAN_STATS")) {
     int nbig = 0;
-    for (int g = 0; g < nsn; ++g) nbig += vnrb[g] * vncb[g] > 1;
-    fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) tasks %d\n",
-            name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(), ntiles,
-            100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), ntasks);
+    for (int g = 0; g < nsn; ++g) nbig += !single[g];
+    fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) tasks %d "
+            "clusters %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(), ntiles,
+            100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), ntasks, (int)clusters.size());
     for (int l = 0; l < fp.nlevels; ++l) {
       long long ent = 0, emax = 0;
       int ncmax = 0, nrmax = 0, tcount = 0, big = 0;
@@ -160,7 +227,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         ncmax = std::max(ncmax, (int)nc);
         nrmax = std::max(nrmax, (int)(nc + no));
         tcount += (int)sn_tiles[g].size();
-        big += vnrb[g] * vncb[g] > 1;
+        big += !single[g];
       }
       fprintf(stderr, "  level %2d: sn %6d (big %4d) entries %10lld max %8lld ncmax %5d nrmax %5d tiles %6d\n", l,
               fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, emax, ncmax, nrmax, tcount);
@@ -190,6 +257,8 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.P = plan();
   S.dinv = dinv.p;
   S.tasks = tasks.p;
+  S.tt_ptr = tt_ptr.p;
+  S.task_tiles = task_tiles.p;
   S.ntasks = ntasks;
   S.total_bwd = total_bwd;
   S.parent = parent.p;

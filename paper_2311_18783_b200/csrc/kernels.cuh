@@ -94,12 +94,20 @@ enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_T0, SW_TSUM, 
 constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 4096;   // doubles per tile (32 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
+constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
+constexpr int64_t kClusterMax = 32768;  // stored entries of a subtree swept by one task
 constexpr int kSweepSmemDoubles = 2 * kTileMax + 2 * kVecMax + kSweepThreads;
 
 struct SweepDev {
   PlanDev P;
   const double* dinv;
-  const int4* tasks;             // {type 0 fwd tile / 1 bwd tile / 2 prolong / 3 assemble, idx, lo, hi}
+  // tasks {type, a, b, c}: 0 fwd tile (a = tile) / 1 bwd tile / 2 prolong [b, c) /
+  // 3 assemble (a = supernode) / 4 cluster fwd (a = cluster root, b = wait for its
+  // children) / 5 cluster bwd (a = cluster root); tiles streamed by a task:
+  // task_tiles[tt_ptr[t] .. tt_ptr[t+1])
+  const int4* tasks;
+  const int* tt_ptr;
+  const int* task_tiles;
   int ntasks;
   int total_bwd;                 // backward column blocks per launch
   const int* parent;             // supernode parent (-1 root)

@@ -213,8 +213,6 @@ __device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, con
 
 __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   extern __shared__ __align__(128) double sm[];
-  double* const stage0 = sm;
-  double* const stage1 = sm + kTileMax;
   double* const vec = sm + 2 * kTileMax;   // kVecMax
   double* const vec2 = vec + kVecMax;      // kVecMax
   double* const red = vec2 + kVecMax;      // kSweepThreads
@@ -236,129 +234,104 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
 #define STAT_MARK(slot) \
   if (S.stats && tid == 0) { long long c_ = clock64(); st_acc[(slot)] += c_ - c_prev; c_prev = c_; }
 
-  // thread 0: take a ticket and start streaming the tile its task reads
-  auto grab = [&](int slot, int buf) {
-    const int t = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
-    s_next[slot] = t;
-    if (t < S.ntasks) {
-      const int4 tk = S.tasks[t];
-      if (tk.x == 0 || tk.x == 1) {
-        const int4 tl = S.tiles[tk.y];
-        const TileGeo G = geo(S, tl.x, tl.y, tl.z);
-        const uint32_t bytes = (uint32_t)(((G.rows * G.cols + 1) & ~1) * sizeof(double));
-        bulk_load(buf ? stage1 : stage0, S.Lt + S.tile_off[tk.y], bytes, &mbar[buf]);
-      }
-    }
+  // thread 0 helpers: start streaming a tile into a stage buffer
+  auto prefetch = [&](int tile, int b) {
+    const int4 tl = S.tiles[tile];
+    const TileGeo G = geo(S, tl.x, tl.y, tl.z);
+    const uint32_t bytes = (uint32_t)(((G.rows * G.cols + 1) & ~1) * sizeof(double));
+    bulk_load(sm + b * kTileMax, S.Lt + S.tile_off[tile], bytes, &mbar[b]);
   };
-  if (tid == 0) grab(0, 0);
+  auto first_tile = [&](int t) -> int {
+    if (t >= S.ntasks) return -1;
+    const int a = S.tt_ptr[t];
+    return a < S.tt_ptr[t + 1] ? S.task_tiles[a] : -1;
+  };
+  int tn = 0;  // thread 0: the look-ahead ticket
+  if (tid == 0) {
+    const int t0 = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
+    s_next[0] = t0;
+    const int ft = first_tile(t0);
+    if (ft >= 0) prefetch(ft, 0);
+  }
   __syncthreads();
-  uint32_t par0 = 0u, par1 = 0u;
+  uint32_t par[2] = {0u, 0u};
   int it = 0, buf = 0;
+  // wait for the tile in `buf` and issue the next one of the stream into buf ^ 1
+  auto next_tile_and_wait = [&](int k, int kend) {
+    if (tid == 0) {
+      const int nxt = k + 1 < kend ? S.task_tiles[k + 1] : first_tile(tn);
+      if (nxt >= 0) prefetch(nxt, buf ^ 1);
+    }
+    mbar_wait(&mbar[buf], par[buf]);
+    par[buf] ^= 1u;
+  };
   for (;;) {
     const int t = s_next[it & 1];
     if (t >= S.ntasks) break;
     const int4 tk = S.tasks[t];
     const int type = tk.x;
-    const bool tiled = type == 0 || type == 1;
-    if (tid == 0) grab((it + 1) & 1, tiled ? buf ^ 1 : buf);  // next tile streams meanwhile
+    const int ka = S.tt_ptr[t], kb = S.tt_ptr[t + 1];
+    if (tid == 0) {
+      tn = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
+      s_next[(it + 1) & 1] = tn;
+      if (ka == kb) {  // no tile of ours in flight: the next task's first tile goes to buf
+        const int ft = first_tile(tn);
+        if (ft >= 0) prefetch(ft, buf);
+      }
+    }
     STAT_MARK(8);
-    double* const T = buf ? stage1 : stage0;
-    auto tile_ready = [&]() {
-      if (buf) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
-      else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
-    };
+    double* const T = sm + buf * kTileMax;
 
     if (type == 0) {
-      // ============================================ forward tile
+      // ============================================ forward tile of a big supernode
       const int4 tl = S.tiles[tk.y];
       const int g = tl.x, rb = tl.y, cb = tl.z;
       const TileGeo G = geo(S, g, rb, cb);
       const i64 col0 = P.sn_col0[g];
-      const bool big = G.nrb * G.ncb > 1;
-      if (!big) {
-        const bool ok = wait_children(S, g, cur, &s_flag);
-        STAT_MARK(0);
-        if (ok) {
-          // t = [b_c ; 0] + extend-add of the children's update vectors
-          double* tc = vec;
-          double* to = vec2;
-          for (int k = tid; k < G.nc; k += kSweepThreads)
-            tc[k] = S.gmap ? __ldg(S.b + __ldg(S.gmap + col0 + k)) : __ldg(S.b + col0 + k);
-          for (int k = tid; k < G.nr - G.nc; k += kSweepThreads) to[k] = 0.0;
-          __syncthreads();
-          for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
-            const int c = P.child_list[ci];
-            const int noc = P.sn_noff[c];
-            const double* u = S.upd + P.sn_uptr[c];
-            const int* rm = P.relmap + P.sn_rowptr[c];
-            for (int a = tid; a < noc; a += kSweepThreads) {
-              const int pos = rm[a];
-              const double val = __ldcg(u + a);
-              if (pos < G.nc) tc[pos] += val;
-              else to[pos - G.nc] += val;
-            }
-            __syncthreads();
-          }
+      const bool ok = wait_one(&S.asm_cnt[g], cur, S.ctl, &s_flag);
+      STAT_MARK(0);
+      if (ok) {
+        const double* tg = S.tg + S.sn_tg[g] + cb * G.CB;
+        for (int k = tid; k < G.cols; k += kSweepThreads) vec[k] = __ldcg(tg + k);
+        __syncthreads();
+      }
+      next_tile_and_wait(ka, kb);
+      if (ok) {
+        double* fp = S.fpart + S.sn_fpart[g] + (i64)cb * G.nr + (i64)rb * G.RB;
+        tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) { fp[i] = y; });
+        __syncthreads();
+        const int rend = min(G.nr, (rb + 1) * G.RB);
+        const int ntl = min(G.ncb, (rend + G.CB - 1) / G.CB);
+        if (tid == 0) {
+          __threadfence();
+          const unsigned long long old = atomicAdd(&S.rb_cnt[S.sn_rbc[g] + rb], 1ull);
+          s_flag = (old + 1 == cur * (unsigned long long)ntl);
+          __threadfence();
         }
-        tile_ready();
-        if (ok) {
-          double* const xf = S.xf + col0;
-          const double* const dinv = S.dinv + col0;
-          double* const upd = S.upd + P.sn_uptr[g];
-          const int nc = G.nc;
-          tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) {
-            if (i < nc) xf[i] = __ldg(dinv + i) * y;
-            else upd[i - nc] = vec2[i - nc] - y;
-          });
+        __syncthreads();
+        if (s_flag) {
+          // last tile of the row block: combine partial sums in column-block order
+          const double* fb = S.fpart + S.sn_fpart[g] + (i64)rb * G.RB;
+          const double* tg = S.tg + S.sn_tg[g] + (i64)rb * G.RB;
+          for (int i = tid; i < G.rows; i += kSweepThreads) {
+            double s = 0.0;
+            for (int q = 0; q < ntl; ++q) s += __ldcg(fb + (i64)q * G.nr + i);
+            const int r = rb * G.RB + i;
+            if (r < G.nc) S.xf[col0 + r] = __ldg(S.dinv + col0 + r) * s;
+            else S.upd[P.sn_uptr[g] + (r - G.nc)] = __ldcg(tg + i) - s;
+          }
           __syncthreads();
           if (tid == 0) signal_add(&S.fwd_cnt[g]);
         }
-      } else {
-        const bool ok = wait_one(&S.asm_cnt[g], cur, S.ctl, &s_flag);
-        STAT_MARK(0);
-        if (ok) {
-          const double* tg = S.tg + S.sn_tg[g] + cb * G.CB;
-          for (int k = tid; k < G.cols; k += kSweepThreads) vec[k] = __ldcg(tg + k);
-          __syncthreads();
-        }
-        tile_ready();
-        if (ok) {
-          double* fp = S.fpart + S.sn_fpart[g] + (i64)cb * G.nr + (i64)rb * G.RB;
-          tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) { fp[i] = y; });
-          __syncthreads();
-          const int rend = min(G.nr, (rb + 1) * G.RB);
-          const int ntl = min(G.ncb, (rend + G.CB - 1) / G.CB);
-          if (tid == 0) {
-            __threadfence();
-            const unsigned long long old = atomicAdd(&S.rb_cnt[S.sn_rbc[g] + rb], 1ull);
-            s_flag = (old + 1 == cur * (unsigned long long)ntl);
-            __threadfence();
-          }
-          __syncthreads();
-          if (s_flag) {
-            // last tile of the row block: combine partial sums in column-block order
-            const double* fb = S.fpart + S.sn_fpart[g] + (i64)rb * G.RB;
-            const double* tg = S.tg + S.sn_tg[g] + (i64)rb * G.RB;
-            for (int i = tid; i < G.rows; i += kSweepThreads) {
-              double s = 0.0;
-              for (int q = 0; q < ntl; ++q) s += __ldcg(fb + (i64)q * G.nr + i);
-              const int r = rb * G.RB + i;
-              if (r < G.nc) S.xf[col0 + r] = __ldg(S.dinv + col0 + r) * s;
-              else S.upd[P.sn_uptr[g] + (r - G.nc)] = __ldcg(tg + i) - s;
-            }
-            __syncthreads();
-            if (tid == 0) signal_add(&S.fwd_cnt[g]);
-          }
-        }
       }
+      buf ^= 1;
       STAT_MARK(1);
     } else if (type == 1) {
-      // ============================================ backward tile
+      // ============================================ backward tile of a big supernode
       const int4 tl = S.tiles[tk.y];
       const int g = tl.x, rb = tl.y, cb = tl.z;
       const TileGeo G = geo(S, g, rb, cb);
       const i64 col0 = P.sn_col0[g];
-      const bool big = G.nrb * G.ncb > 1;
       const int p = S.parent[g];
       const bool ok = p >= 0 ? wait_one(&S.bwd_cnt[p], cur * (unsigned long long)S.sn_ncb[p], S.ctl, &s_flag)
                              : wait_one(&S.fwd_cnt[g], cur * (unsigned long long)G.nrb, S.ctl, &s_flag);
@@ -371,43 +344,116 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         }
         __syncthreads();
       }
-      tile_ready();
+      next_tile_and_wait(ka, kb);
       if (ok) {
-        if (!big) {
-          double* const xb = S.xb + col0;
-          tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
+        double* bp = S.bpart + S.sn_bpart[g] + (i64)rb * G.nc + (i64)cb * G.CB;
+        tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { bp[j] = y; });
+        __syncthreads();
+        const int rb0 = (cb * G.CB) / G.RB;
+        if (tid == 0) {
+          __threadfence();
+          const unsigned long long old = atomicAdd(&S.cb_cnt[S.sn_cbc[g] + cb], 1ull);
+          s_flag = (old + 1 == cur * (unsigned long long)(G.nrb - rb0));
+          __threadfence();
+        }
+        __syncthreads();
+        if (s_flag) {
+          // last tile of the column block: combine partial sums in row-block order
+          const double* bb = S.bpart + S.sn_bpart[g] + (i64)cb * G.CB;
+          for (int j = tid; j < G.cols; j += kSweepThreads) {
+            double s = 0.0;
+            for (int q = rb0; q < G.nrb; ++q) s += __ldcg(bb + (i64)q * G.nc + j);
+            S.xb[col0 + cb * G.CB + j] = s;
+          }
           __syncthreads();
           if (tid == 0) {
             signal_add(&S.bwd_cnt[g]);
             atomicAdd(&S.ctl[SW_BWD_DONE], 1ull);
           }
-        } else {
-          double* bp = S.bpart + S.sn_bpart[g] + (i64)rb * G.nc + (i64)cb * G.CB;
-          tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { bp[j] = y; });
-          __syncthreads();
-          const int rb0 = (cb * G.CB) / G.RB;
-          if (tid == 0) {
-            __threadfence();
-            const unsigned long long old = atomicAdd(&S.cb_cnt[S.sn_cbc[g] + cb], 1ull);
-            s_flag = (old + 1 == cur * (unsigned long long)(G.nrb - rb0));
-            __threadfence();
+        }
+      }
+      buf ^= 1;
+      STAT_MARK(3);
+    } else if (type == 4) {
+      // ============================================ forward of a cluster of small
+      // supernodes (a subtree, or one supernode whose children were waited for),
+      // postorder, one CTA: no inter-CTA synchronisation inside the cluster
+      bool ok = true;
+      if (tk.z) ok = wait_children(S, tk.y, cur, &s_flag);
+      else if (tid == 0 && *(volatile unsigned long long*)&S.ctl[SW_ABORT]) ok = false;
+      STAT_MARK(0);
+      for (int k = ka; k < kb; ++k) {
+        const int4 tl = S.tiles[S.task_tiles[k]];
+        const int g = tl.x, cb = tl.z;
+        const TileGeo G = geo(S, g, 0, cb);
+        const i64 col0 = P.sn_col0[g];
+        if (cb == 0 && ok) {
+          // t = [b_c ; 0] + extend-add of the children's update vectors; acc = 0
+          for (int q = tid; q < G.nr; q += kSweepThreads) {
+            vec[q] = q < G.nc ? (S.gmap ? __ldg(S.b + __ldg(S.gmap + col0 + q)) : __ldg(S.b + col0 + q)) : 0.0;
+            vec2[q] = 0.0;
           }
           __syncthreads();
-          if (s_flag) {
-            // last tile of the column block: combine partial sums in row-block order
-            const double* bb = S.bpart + S.sn_bpart[g] + (i64)cb * G.CB;
-            for (int j = tid; j < G.cols; j += kSweepThreads) {
-              double s = 0.0;
-              for (int q = rb0; q < G.nrb; ++q) s += __ldcg(bb + (i64)q * G.nc + j);
-              S.xb[col0 + cb * G.CB + j] = s;
-            }
+          for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
+            const int c = P.child_list[ci];
+            const int noc = P.sn_noff[c];
+            const double* u = S.upd + P.sn_uptr[c];
+            const int* rm = P.relmap + P.sn_rowptr[c];
+            for (int a = tid; a < noc; a += kSweepThreads) vec[rm[a]] += __ldcg(u + a);
             __syncthreads();
-            if (tid == 0) {
-              signal_add(&S.bwd_cnt[g]);
-              atomicAdd(&S.ctl[SW_BWD_DONE], 1ull);
-            }
           }
         }
+        next_tile_and_wait(k, kb);
+        if (ok) {
+          const double* v = vec + cb * G.CB;
+          tile_matvec(sm + buf * kTileMax, G.rows, G.cols, v, red,
+                      [&](int i, double y) { vec2[i] += y; });
+          __syncthreads();
+          if (cb == G.ncb - 1) {
+            double* const xf = S.xf + col0;
+            double* const upd = S.upd + P.sn_uptr[g];
+            for (int i = tid; i < G.nr; i += kSweepThreads) {
+              if (i < G.nc) xf[i] = __ldg(S.dinv + col0 + i) * vec2[i];
+              else upd[i - G.nc] = vec[i] - vec2[i];
+            }
+            __syncthreads();
+            if (tid == 0) signal_add(&S.fwd_cnt[g]);
+          }
+        }
+        buf ^= 1;
+      }
+      STAT_MARK(1);
+    } else if (type == 5) {
+      // ============================================ backward of a cluster (reverse
+      // postorder: every ancestor inside the cluster is done before its children)
+      const int g0 = tk.y;
+      const int p0 = S.parent[g0];
+      const bool ok = p0 >= 0 ? wait_one(&S.bwd_cnt[p0], cur * (unsigned long long)S.sn_ncb[p0], S.ctl, &s_flag)
+                              : wait_one(&S.fwd_cnt[g0], cur * (unsigned long long)S.sn_nrb[g0], S.ctl, &s_flag);
+      STAT_MARK(2);
+      for (int k = ka; k < kb; ++k) {
+        const int4 tl = S.tiles[S.task_tiles[k]];
+        const int g = tl.x, cb = tl.z;
+        const TileGeo G = geo(S, g, 0, cb);
+        const i64 col0 = P.sn_col0[g];
+        if (cb == 0 && ok) {
+          const i64* rows = P.offrows + P.sn_rowptr[g];
+          for (int i = tid; i < G.nr; i += kSweepThreads)
+            vec[i] = i < G.nc ? __ldcg(S.xf + col0 + i) : -__ldcg(S.xb + rows[i - G.nc]);
+          __syncthreads();
+        }
+        next_tile_and_wait(k, kb);
+        if (ok) {
+          double* const xb = S.xb + col0 + cb * G.CB;
+          tile_matvec_t(sm + buf * kTileMax, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
+          __syncthreads();
+          if (cb == G.ncb - 1 && tid == 0) {
+            __threadfence();
+            atomicAdd(&S.bwd_cnt[g], (unsigned long long)G.ncb);
+            atomicAdd(&S.ctl[SW_BWD_DONE], (unsigned long long)G.ncb);
+          }
+        }
+        buf ^= 1;
       }
       STAT_MARK(3);
     } else if (type == 3) {
@@ -451,7 +497,6 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     }
     if (S.stats && tid == 0) st_acc[9] += 1;
     __syncthreads();
-    if (tiled) buf ^= 1;
     ++it;
   }
 #undef STAT_MARK
