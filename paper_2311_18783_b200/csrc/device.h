@@ -78,9 +78,10 @@ struct DevFactor {
   // persistent sweep (sweep.cu): tiles and schedule
   DBuf<int4> tasks, tiles;
   DBuf<int64_t> tile_off, sn_fpart, sn_bpart, sn_tg;
-  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc, tt_ptr, task_tiles;
+  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc, tt_ptr;
+  DBuf<int4> tdesc;
   DBuf<double> Lt, fpart, bpart, tg;
-  DBuf<unsigned long long> fwd_cnt, bwd_cnt, rb_cnt, cb_cnt, asm_cnt, ctl, stats;
+  DBuf<unsigned long long> fwd_cnt, bwd_cnt, rb_cnt, cb_cnt, asm_cnt, ctl, stats, trace;
   int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, ntiles = 0, sweep_grid = 0;
   int64_t lt_size = 0;
   const int64_t* pro_ptr = nullptr;

@@ -175,7 +175,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       std::vector<int> ts;
       for (auto it2 = clusters[c].members.rbegin(); it2 != clusters[c].members.rend(); ++it2)
         ts.insert(ts.end(), sn_tiles[*it2].begin(), sn_tiles[*it2].end());
-      add_task(make_int4(5, clusters[c].root, 0, 0), ts);
+      int ncbs = 0;
+      for (int g : clusters[c].members) ncbs += vncb[g];
+      add_task(make_int4(5, clusters[c].root, clusters[c].wait, ncbs), ts);
     }
   }
   ntasks_noprolong = (int)tk.size();
@@ -188,7 +190,19 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   ntasks = (int)tk.size();
   tasks.upload(tk);
   tt_ptr.upload(ttp);
-  task_tiles.upload(ttl);
+  {
+    std::vector<int4> td(ttl.size());
+    for (size_t k = 0; k < ttl.size(); ++k) {
+      const int t = ttl[k];
+      const int4 q = tl[t];
+      const int g = q.x;
+      const int nr = fp.sn_ncol[g] + fp.sn_noff[g], nc = fp.sn_ncol[g];
+      const int rows = std::min(vRB[g], nr - q.y * vRB[g]), cols = std::min(vCB[g], nc - q.z * vCB[g]);
+      const int bytes = (int)((((int64_t)rows * cols + 1) & ~1LL) * (int64_t)sizeof(double));
+      td[k] = make_int4(t, bytes, (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32));
+    }
+    tdesc.upload(td);
+  }
   tiles.upload(tl);
   tile_off.upload(toff);
   sn_RB.upload(vRB); sn_CB.upload(vCB); sn_nrb.upload(vnrb); sn_ncb.upload(vncb);
@@ -205,6 +219,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   ctl.alloc(dev::SW_COUNT);
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
+  if (getenv("MDD_SWEEP_TRACE")) {
+    trace.alloc((size_t)4 * ntasks);
+    CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
+  }
   if (getenv("MDD_SWEEP_STATS")) {
     stats.alloc(10);
     CUDA_CHECK(cudaMemset(stats.p, 0, 10 * sizeof(unsigned long long)));
@@ -258,7 +276,7 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.dinv = dinv.p;
   S.tasks = tasks.p;
   S.tt_ptr = tt_ptr.p;
-  S.task_tiles = task_tiles.p;
+  S.tdesc = tdesc.p;
   S.ntasks = ntasks;
   S.total_bwd = total_bwd;
   S.parent = parent.p;
@@ -283,10 +301,26 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.out = nullptr;
   S.stop = nullptr;
   S.stats = stats.p;
+  S.trace = trace.p;
   return S;
 }
 
 DevFactor::~DevFactor() {
+  if (trace.p && getenv("MDD_SWEEP_TRACE") && !name.empty()) {
+    std::vector<unsigned long long> v(trace.n);
+    std::vector<int4> tk(ntasks);
+    if (cudaMemcpy(v.data(), trace.p, v.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
+        cudaMemcpy(tk.data(), tasks.p, tk.size() * sizeof(int4), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      std::string path = std::string(getenv("MDD_SWEEP_TRACE")) + "/trace_" + name + ".bin";
+      if (FILE* f = fopen(path.c_str(), "wb")) {
+        int nt = ntasks;
+        fwrite(&nt, sizeof(int), 1, f);
+        fwrite(tk.data(), sizeof(int4), tk.size(), f);
+        fwrite(v.data(), 8, v.size(), f);
+        fclose(f);
+      }
+    }
+  }
   if (stats.p) {
     unsigned long long v[10];
     if (cudaMemcpy(v, stats.p, sizeof(v), cudaMemcpyDeviceToHost) == cudaSuccess)

@@ -107,7 +107,7 @@ struct SweepDev {
   // task_tiles[tt_ptr[t] .. tt_ptr[t+1])
   const int4* tasks;
   const int* tt_ptr;
-  const int* task_tiles;
+  const int4* tdesc;             // per task-ordered tile: {tile, bytes, offset lo, offset hi}
   int ntasks;
   int total_bwd;                 // backward column blocks per launch
   const int* parent;             // supernode parent (-1 root)
@@ -143,6 +143,7 @@ struct SweepDev {
   double* out;                   // prolongation target (global)
   const int* stop;               // PCG stop flag (nullable): set -> no-op launch
   unsigned long long* stats;     // optional cycle accounting (MDD_SWEEP_STATS=1)
+  unsigned long long* trace;     // optional per-task timeline (MDD_SWEEP_TRACE=dir)
 };
 __global__ void k_sweep(SweepDev S);
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,

@@ -232,26 +232,28 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   long long st_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long c_prev = clock64();
 #define STAT_MARK(slot) \
-  if (S.stats && tid == 0) { long long c_ = clock64(); st_acc[(slot)] += c_ - c_prev; c_prev = c_; }
+  if (S.stats && tid == 0) { long long c_ = clock64(); st_acc[(slot)] += c_ - c_prev; c_prev = c_; } \
+  if (S.trace && tid == 0 && ((slot) == 0 || (slot) == 2 || (slot) == 4 || (slot) == 6)) \
+    S.trace[4 * (size_t)t + 1] = globaltimer();
 
-  // thread 0 helpers: start streaming a tile into a stage buffer
-  auto prefetch = [&](int tile, int b) {
-    const int4 tl = S.tiles[tile];
-    const TileGeo G = geo(S, tl.x, tl.y, tl.z);
-    const uint32_t bytes = (uint32_t)(((G.rows * G.cols + 1) & ~1) * sizeof(double));
-    bulk_load(sm + b * kTileMax, S.Lt + S.tile_off[tile], bytes, &mbar[b]);
+  // thread 0 helpers: start streaming a tile into a stage buffer.  tdesc[k] =
+  // {tile, bytes, offset lo, offset hi} in task order: one load per prefetch
+  auto prefetch_k = [&](int k, int b) {
+    const int4 d = S.tdesc[k];
+    const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
+    bulk_load(sm + b * kTileMax, S.Lt + off, (uint32_t)d.y, &mbar[b]);
   };
-  auto first_tile = [&](int t) -> int {
+  auto first_k = [&](int t) -> int {
     if (t >= S.ntasks) return -1;
     const int a = S.tt_ptr[t];
-    return a < S.tt_ptr[t + 1] ? S.task_tiles[a] : -1;
+    return a < S.tt_ptr[t + 1] ? a : -1;
   };
   int tn = 0;  // thread 0: the look-ahead ticket
   if (tid == 0) {
     const int t0 = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
     s_next[0] = t0;
-    const int ft = first_tile(t0);
-    if (ft >= 0) prefetch(ft, 0);
+    const int fk = first_k(t0);
+    if (fk >= 0) prefetch_k(fk, 0);
   }
   __syncthreads();
   uint32_t par[2] = {0u, 0u};
@@ -259,8 +261,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   // wait for the tile in `buf` and issue the next one of the stream into buf ^ 1
   auto next_tile_and_wait = [&](int k, int kend) {
     if (tid == 0) {
-      const int nxt = k + 1 < kend ? S.task_tiles[k + 1] : first_tile(tn);
-      if (nxt >= 0) prefetch(nxt, buf ^ 1);
+      const int nk = k + 1 < kend ? k + 1 : first_k(tn);
+      if (nk >= 0) prefetch_k(nk, buf ^ 1);
     }
     mbar_wait(&mbar[buf], par[buf]);
     par[buf] ^= 1u;
@@ -275,11 +277,15 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       tn = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
       s_next[(it + 1) & 1] = tn;
       if (ka == kb) {  // no tile of ours in flight: the next task's first tile goes to buf
-        const int ft = first_tile(tn);
-        if (ft >= 0) prefetch(ft, buf);
+        const int fk = first_k(tn);
+        if (fk >= 0) prefetch_k(fk, buf);
       }
     }
     STAT_MARK(8);
+    if (S.trace && tid == 0) {
+      S.trace[4 * (size_t)t] = globaltimer();
+      S.trace[4 * (size_t)t + 3] = ((unsigned long long)blockIdx.x << 8) | (unsigned long long)type;
+    }
     double* const T = sm + buf * kTileMax;
 
     if (type == 0) {
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       else if (tid == 0 && *(volatile unsigned long long*)&S.ctl[SW_ABORT]) ok = false;
       STAT_MARK(0);
       for (int k = ka; k < kb; ++k) {
-        const int4 tl = S.tiles[S.task_tiles[k]];
+        const int4 tl = S.tiles[S.tdesc[k].x];
         const int g = tl.x, cb = tl.z;
         const TileGeo G = geo(S, g, 0, cb);
         const i64 col0 = P.sn_col0[g];
@@ -417,7 +423,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
               else upd[i - G.nc] = vec[i] - vec2[i];
             }
             __syncthreads();
-            if (tid == 0) signal_add(&S.fwd_cnt[g]);
+            // only the cluster root is waited for from outside the cluster
+            if (tid == 0 && g == tk.y) signal_add(&S.fwd_cnt[g]);
           }
         }
         buf ^= 1;
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
                               : wait_one(&S.fwd_cnt[g0], cur * (unsigned long long)S.sn_nrb[g0], S.ctl, &s_flag);
       STAT_MARK(2);
       for (int k = ka; k < kb; ++k) {
-        const int4 tl = S.tiles[S.task_tiles[k]];
+        const int4 tl = S.tiles[S.tdesc[k].x];
         const int g = tl.x, cb = tl.z;
         const TileGeo G = geo(S, g, 0, cb);
         const i64 col0 = P.sn_col0[g];
@@ -447,13 +454,17 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           double* const xb = S.xb + col0 + cb * G.CB;
           tile_matvec_t(sm + buf * kTileMax, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
           __syncthreads();
-          if (cb == G.ncb - 1 && tid == 0) {
+          // children outside the cluster exist only for a single-supernode cluster
+          if (cb == G.ncb - 1 && tid == 0 && tk.z) {
             __threadfence();
             atomicAdd(&S.bwd_cnt[g], (unsigned long long)G.ncb);
-            atomicAdd(&S.ctl[SW_BWD_DONE], (unsigned long long)G.ncb);
           }
         }
         buf ^= 1;
+      }
+      if (tid == 0 && ok) {
+        __threadfence();
+        atomicAdd(&S.ctl[SW_BWD_DONE], (unsigned long long)tk.w);  // column blocks of the cluster
       }
       STAT_MARK(3);
     } else if (type == 3) {
@@ -496,6 +507,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       STAT_MARK(5);
     }
     if (S.stats && tid == 0) st_acc[9] += 1;
+    if (S.trace && tid == 0) S.trace[4 * (size_t)t + 2] = globaltimer();
     __syncthreads();
     ++it;
   }

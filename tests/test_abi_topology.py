@@ -70,3 +70,21 @@ def test_bad_arguments_fail_loudly():
     w = workloads.custom(5, 4, 4, 2, 2, 2)   # 5 not divisible by 2
     with pytest.raises(MDDError):
         T(w, "sub_ptr")
+
+
+def test_topology_bit_exact_c1_full_size():
+    # BASELINE configs[1] at full size (220k free edges): numbering, the pattern
+    # of A and every subdomain's dof list N_i agree bit-for-bit with the oracle
+    from paper_2311_18783_b200 import topology_array as T
+    w = workloads.make("c1")
+    m = om.mesh_of(w)
+    assert np.array_equal(T(w, "edge_tail"), m.edges[:, 0])
+    assert np.array_equal(T(w, "edge_head"), m.edges[:, 1])
+    assert np.array_equal(T(w, "free_edges"), m.free_edges)
+    A, _, _ = assembly.system_matrix(m, w.mu_inv, w.eps, w.gamma)
+    assert np.array_equal(T(w, "A_ptr"), A.indptr)
+    assert np.array_equal(T(w, "A_idx"), A.indices)
+    dec = dd.decompose(m, w.px, w.py, w.pz, w.overlap)
+    ptr, dofs = T(w, "sub_ptr"), T(w, "sub_dofs")
+    for i, d in enumerate(dec.dofs):
+        assert np.array_equal(dofs[ptr[i]:ptr[i + 1]], d)

@@ -1,0 +1,93 @@
+"""GPU checks at BASELINE's full c1 size (the configuration bench.py times), where
+the oracle cannot run end to end: sampled outputs the oracle computes one by one
+(a single subdomain's local solve, the true residual with the oracle's own A) and
+properties that hold at any size (P0 = QA is an A-orthogonal projection, M
+symmetric)."""
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+import workloads
+from oracle import assembly, dd, mesh as om
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1():
+    from paper_2311_18783_b200 import MaxwellDD
+    w = workloads.make("c1")
+    G = MaxwellDD(w)
+    m = om.mesh_of(w)
+    A, _, _ = assembly.system_matrix(m, w.mu_inv, w.eps, w.gamma)
+    dec = dd.decompose(m, w.px, w.py, w.pz, w.overlap)
+    return w, G, A.tocsr(), dec
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def test_assembled_matrix_full_size(c1):
+    w, G, A, dec = c1
+    assert np.array_equal(G.int_array("A_ptr"), A.indptr)
+    assert np.abs(G.double_array("A_val") - A.data).max() <= 1e-13 * np.abs(A.data).max()
+
+
+@pytest.mark.parametrize("sub", [0, 21, 63])
+def test_single_subdomain_local_solve(c1, sub):
+    # r supported on dofs that only subdomain `sub` owns (multiplicity 1) has
+    # R_j r = 0 for j != sub, so M_AS r = R_sub^T A_sub^{-1} R_sub r (eq. AS)
+    w, G, A, dec = c1
+    d = dec.dofs[sub]
+    own = d[dec.mult[d] == 1]
+    rng = np.random.default_rng(sub)
+    r = np.zeros(A.shape[0])
+    r[own] = rng.standard_normal(len(own))
+    z = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    G.apply_local(dev(r), z)
+    Ai = A[d][:, d].tocsc()
+    zi = spla.splu(Ai).solve(r[d])
+    ref = np.zeros_like(r)
+    ref[d] = zi
+    zg = z.cpu().numpy()
+    # kappa(A_i) ~ 1e11 for the contrast-1e4, gamma-1e-4 recipe (R9)
+    assert np.linalg.norm(zg - ref) <= 1e-4 * np.linalg.norm(ref)
+    # the residual of the local system is at round-off level
+    res = Ai @ zg[d] - r[d]
+    assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(r[d])
+    outside = np.setdiff1d(np.arange(len(r)), d)
+    assert not zg[outside].any()
+
+
+def test_coarse_projection_properties(c1):
+    w, G, A, dec = c1
+    n = A.shape[0]
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(n)
+
+    def Q(x):
+        y = torch.empty(n, dtype=torch.float64, device="cuda")
+        G.apply_coarse(dev(x), y)
+        return y.cpu().numpy()
+
+    p = Q(A @ v)
+    pp = Q(A @ p)
+    nA = lambda x: np.sqrt(x @ (A @ x))
+    assert nA(pp - p) <= 1e-5 * nA(p)          # P0^2 = P0 (kappa(E) ~ 1e13, static pivots)
+    u = rng.standard_normal(n)
+    assert abs(u @ Q(v) - v @ Q(u)) <= 1e-10 * np.linalg.norm(Q(v)) * np.linalg.norm(u)
+
+
+def test_pcg_full_size(c1):
+    w, G, A, dec = c1
+    f = workloads.rhs(A.shape[0], w.f_seed)
+    x = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    it, rel, ok = G.solve(dev(f), x, tol=1e-8)
+    assert ok and rel <= 1e-8 and 10 <= it <= 200
+    xh = x.cpu().numpy()
+    # true residual with the oracle's A: CG's attainable accuracy at kappa(A) ~ 1e11
+    assert np.linalg.norm(f - A @ xh) <= 1e-3 * np.linalg.norm(f)
+    it2, rel2, ok2 = G.solve(dev(f), x, tol=1e-8)
+    assert it2 == it and np.array_equal(x.cpu().numpy(), xh)   # bit-reproducible
