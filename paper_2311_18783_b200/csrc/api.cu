@@ -246,13 +246,13 @@ struct mdd_solver {
   // z = sum_i R_i^T A_i^{-1} R_i r: one persistent launch (gather, fwd, D^{-1}, bwd,
   // prolongation)
   void apply_local(const double* rr, double* zz) {
-    loc.sweep(rr, gmap.p, zz, stream, state.p);
+    loc.sweep(rr, zz, stream, state.p);
     launches += 1;
   }
   void apply_coarse(const double* v, double* y) {
     dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
                                                                  Zt_val.p, v, xc.p, state.p);
-    crs.sweep(xc.p, nullptr, nullptr, stream, state.p);
+    crs.sweep(xc.p, nullptr, stream, state.p);
     dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
                                                                          crs.xb.p, y, state.p);
     launches += 3;
@@ -484,7 +484,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         pos[cur[H->dec.sub_dofs[i][k]]++] = fp.iperm_global[fp.sys_off[i] + k];
     H->pro_ptr.upload(pp);
     H->pro_pos.upload(pos);
-    H->loc.upload(n, H->pro_ptr.p, H->pro_pos.p);
+    H->loc.upload(n, H->pro_ptr.p, H->pro_pos.p, &gm);
   }
   H->setup_times[PH_LOCAL_SYMBOLIC] = now_s() - t0;
   t0 = now_s();

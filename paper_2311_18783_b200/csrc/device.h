@@ -75,14 +75,14 @@ struct DevFactor {
   DBuf<int64_t> col0, rowptr, offrows, lptr, uptr, fptr, umptr, child_ptr, asm_ptr, asm_src;
   DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn, parent;
   DBuf<double> L, dinv, upd, xf, xb;
-  // persistent sweep (sweep.cu): tiles and schedule
-  DBuf<int4> tasks, tiles;
-  DBuf<int64_t> tile_off, sn_fpart, sn_bpart, sn_tg;
-  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc, tt_ptr;
-  DBuf<int4> tdesc;
-  DBuf<double> Lt, fpart, bpart, tg;
-  DBuf<unsigned long long> fwd_cnt, bwd_cnt, rb_cnt, cb_cnt, asm_cnt, ctl, stats, trace;
-  int ntasks = 0, ntasks_noprolong = 0, total_bwd = 0, ntiles = 0, sweep_grid = 0;
+  // persistent level-synchronous sweep (sweep.cu)
+  DBuf<int4> phases, mtask, tdesc, tiles;
+  DBuf<int64_t> tile_off, sn_fpart, sn_bpart, vb_off, cptr, cidx, wsrc;
+  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc;
+  DBuf<int32_t> gsrc;
+  DBuf<double> Lt, fpart, bpart, vb;
+  DBuf<unsigned long long> rb_cnt, cb_cnt, ticket, ctl, trace;
+  int nphases = 0, nphases_noprolong = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
   int64_t lt_size = 0;
   const int64_t* pro_ptr = nullptr;
   const int32_t* pro_pos = nullptr;
@@ -92,21 +92,20 @@ struct DevFactor {
   ~DevFactor();
   dev::PlanDev plan() const;
   dev::SweepDev sweep_dev() const;
-  // prolong_n > 0 appends prolongation chunks over prolong_n global dofs
+  // Builds the sweep schedule.  prolong_n > 0 appends the prolongation onto
+  // prolong_n global dofs; gmap_host maps positions to indices of the sweep's
+  // right-hand side (NULL: the right-hand side is indexed by position).
   void upload(int prolong_n = 0, const int64_t* pro_ptr_dev = nullptr,
-              const int32_t* pro_pos_dev = nullptr);
+              const int32_t* pro_pos_dev = nullptr, const std::vector<int32_t>* gmap_host = nullptr);
   // numeric multifrontal factorisation from a device value array `src`; the
   // panels are then re-laid out into the sweep tiles
   int factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
-  // x = A^{-1} b in one persistent launch.  b is gathered through gmap (positions
-  // -> source index) when gmap != NULL; with `out` the result is prolongated to
-  // out[e] = sum of its copies (needs upload(prolong_n > 0)), else it stays in xb
-  // (positions).
-  void sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s,
-             const int* stop = nullptr) const;
+  // x = A^{-1} b in one persistent launch; with `out` the result is prolongated
+  // (out[e] = sum of its copies; needs upload(prolong_n > 0)), else it stays in xb.
+  void sweep(const double* b, double* out, cudaStream_t s, const int* stop = nullptr) const;
   // accumulated device time (ns) and count of sweep launches (SW_TSUM / SW_TCNT)
   void sweep_timing(unsigned long long* ns, unsigned long long* cnt, cudaStream_t s) const;
-  // throws if a sweep aborted (spin timeout); resets the schedule state
+  // throws if a sweep aborted (barrier timeout); resets the schedule state
   void check_abort(cudaStream_t s);
   void reset_counters(cudaStream_t s);
 };

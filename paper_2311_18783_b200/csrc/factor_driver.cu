@@ -29,11 +29,8 @@ dev::PlanDev DevFactor::plan() const {
   return P;
 }
 
-namespace {
-constexpr int kProlongChunk = 2048;
-}  // namespace
-
-void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t* pro_pos_dev) {
+void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t* pro_pos_dev,
+                       const std::vector<int32_t>* gmap_host) {
   col0.upload(fp.sn_col0);
   ncol.upload(fp.sn_ncol);
   noff.upload(fp.sn_noff);
@@ -56,24 +53,23 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   upd.alloc(std::max<int64_t>(fp.usize, 1));
   xf.alloc(std::max<int64_t>(fp.ntot, 1));
   xb.alloc(std::max<int64_t>(fp.ntot, 1));
-  // ---- tile geometry per supernode.  "single": swept by one CTA (column tiles
-  // over all nr rows, accumulated in shared memory); "big": RB x CB tiles spread
-  // over CTAs with partial sums
+  // ---- tile geometry.  "small": one CTA sweeps the whole panel (column tiles over
+  // all nr rows, accumulated in shared memory); "big": RB x CB tiles spread over
+  // CTAs, partial sums combined by the last tile of a row / column block
   const int nsn = fp.nsn;
   std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn), vncb(nsn), vrbc(nsn, 0), vcbc(nsn, 0);
-  std::vector<uint8_t> single(nsn);
-  std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0), vtg(nsn, 0), stored(nsn);
+  std::vector<uint8_t> small(nsn);
+  std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0);
   std::vector<std::vector<int>> sn_tiles(nsn);
   std::vector<int4> tl;
   std::vector<int64_t> toff;
-  int64_t off = 0, nfp = 0, nbp = 0, ntg = 0;
+  int64_t off = 0, nfp = 0, nbp = 0;
   int nrbc = 0, ncbc = 0;
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
-    stored[g] = (int64_t)nr * nc;
-    single[g] = nr <= dev::kVecMax && stored[g] <= dev::kSingleMax;
+    small[g] = nr <= dev::kVecMax && (int64_t)nr * nc <= dev::kSingleMax;
     int RB, CB;
-    if (single[g]) {
+    if (small[g]) {
       RB = nr;
       CB = std::max(1, std::min(nc, dev::kTileMax / nr));
     } else {
@@ -82,10 +78,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     }
     const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
     vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
-    if (!single[g]) {
+    if (!small[g]) {
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;
       vbp[g] = nbp; nbp += (int64_t)nrb * nc;
-      vtg[g] = ntg; ntg += nr;
       vrbc[g] = nrbc; nrbc += nrb;
       vcbc[g] = ncbc; ncbc += ncb;
     }
@@ -102,155 +97,117 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   ntiles = (int)tl.size();
   lt_size = off;
-  // ---- clusters: a single-only subtree of <= kClusterMax stored entries is one
-  // task (postorder); a single supernode above such subtrees is its own cluster
-  std::vector<std::vector<int>> kids(nsn);
-  for (int g = 0; g < nsn; ++g)
-    if (fp.sn_parent[g] >= 0) kids[fp.sn_parent[g]].push_back(g);
-  std::vector<uint8_t> sub_ok(nsn);
-  std::vector<int64_t> sub_sz(nsn);
-  for (int g = 0; g < nsn; ++g) {  // children precede parents
-    bool okg = single[g];
-    int64_t sz = stored[g];
-    for (int c : kids[g]) { okg = okg && sub_ok[c]; sz += sub_sz[c]; }
-    sub_ok[g] = okg;
-    sub_sz[g] = sz;
-  }
-  struct Cl { int root; int wait; std::vector<int> members; };
-  std::vector<Cl> clusters;
-  std::vector<int> bigs;
-  std::vector<int> stack;
-  for (int g = 0; g < nsn; ++g)
-    if (fp.sn_parent[g] < 0) stack.push_back(g);
-  while (!stack.empty()) {
-    const int g = stack.back();
-    stack.pop_back();
-    if (single[g] && sub_ok[g] && sub_sz[g] <= dev::kClusterMax) {
-      Cl c{g, 0, {}};
-      std::vector<int> st{g}, order;
-      while (!st.empty()) {  // preorder, reversed below into a postorder
-        const int v = st.back();
-        st.pop_back();
-        order.push_back(v);
-        for (int k : kids[v]) st.push_back(k);
-      }
-      c.members.assign(order.rbegin(), order.rend());
-      clusters.push_back(std::move(c));
-      continue;
-    }
-    if (single[g]) clusters.push_back(Cl{g, kids[g].empty() ? 0 : 1, {g}});
-    else bigs.push_back(g);
-    for (int k : kids[g]) stack.push_back(k);
-  }
-  // ---- schedule: forward work by level of its top supernode, backward work in
-  // the reverse order, prolongation last.  Every wait targets an earlier ticket.
-  std::vector<std::vector<int>> cl_at(fp.nlevels), big_at(fp.nlevels);
-  for (int c = 0; c < (int)clusters.size(); ++c) cl_at[fp.sn_level[clusters[c].root]].push_back(c);
-  for (int g : bigs) big_at[fp.sn_level[g]].push_back(g);
-  std::vector<int4> tk;
-  std::vector<int> ttp(1, 0), ttl;
-  auto add_task = [&](int4 t, const std::vector<int>& tiles_) {
-    tk.push_back(t);
-    ttl.insert(ttl.end(), tiles_.begin(), tiles_.end());
-    ttp.push_back((int)ttl.size());
+  auto tile_bytes = [&](int t) {
+    const int4 q = tl[t];
+    const int g = q.x, nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
+    const int rows = std::min(vRB[g], nr - q.y * vRB[g]), cols = std::min(vCB[g], nc - q.z * vCB[g]);
+    return (int)((((int64_t)rows * cols + 1) & ~1LL) * (int64_t)sizeof(double));
   };
-  const std::vector<int> none;
+  // ---- per-level row vectors: rows of g at vb_off[g], each level contiguous
+  std::vector<int64_t> vvo(nsn), lev_row(fp.nlevels + 1, 0);
+  int64_t nrows = 0;
   for (int l = 0; l < fp.nlevels; ++l) {
-    for (int c : cl_at[l]) {
-      std::vector<int> ts;
-      for (int g : clusters[c].members) ts.insert(ts.end(), sn_tiles[g].begin(), sn_tiles[g].end());
-      add_task(make_int4(4, clusters[c].root, clusters[c].wait, 0), ts);
-    }
-    for (int g : big_at[l]) {
-      add_task(make_int4(3, g, 0, 0), none);
-      for (int t : sn_tiles[g]) add_task(make_int4(0, t, 0, 0), std::vector<int>{t});
+    lev_row[l] = nrows;
+    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+      const int g = fp.level_sn[k];
+      vvo[g] = nrows;
+      nrows += fp.sn_ncol[g] + fp.sn_noff[g];
     }
   }
-  total_bwd = 0;
-  for (int g = 0; g < nsn; ++g) total_bwd += vncb[g];
+  lev_row[fp.nlevels] = nrows;
+  // forward gather: row -> b index (column rows) and children's update entries
+  std::vector<int32_t> vgsrc(nrows, -1);
+  std::vector<int64_t> vwsrc(nrows);
+  std::vector<std::vector<int64_t>> contrib(nrows);
+  for (int g = 0; g < nsn; ++g) {
+    const int nc = fp.sn_ncol[g], no = fp.sn_noff[g];
+    const int64_t c0 = fp.sn_col0[g];
+    for (int r = 0; r < nc; ++r) {
+      vgsrc[vvo[g] + r] = gmap_host ? (*gmap_host)[c0 + r] : (int32_t)(c0 + r);
+      vwsrc[vvo[g] + r] = c0 + r;
+    }
+    for (int r = 0; r < no; ++r) vwsrc[vvo[g] + nc + r] = -(fp.offrows[fp.sn_rowptr[g] + r]) - 1;
+    for (int64_t ci = fp.child_ptr[g]; ci < fp.child_ptr[g + 1]; ++ci) {
+      const int c = fp.child_list[ci];
+      for (int a = 0; a < fp.sn_noff[c]; ++a)
+        contrib[vvo[g] + fp.relmap[fp.sn_rowptr[c] + a]].push_back(fp.sn_uptr[c] + a);
+    }
+  }
+  std::vector<int64_t> vcptr(nrows + 1, 0), vcidx;
+  for (int64_t q = 0; q < nrows; ++q) {
+    vcidx.insert(vcidx.end(), contrib[q].begin(), contrib[q].end());
+    vcptr[q + 1] = (int64_t)vcidx.size();
+  }
+  std::vector<std::vector<int64_t>>().swap(contrib);
+  // ---- M tasks per level (largest first) and the phase list
+  std::vector<int4> mt, td, ph;
+  std::vector<int> mt_lev(fp.nlevels + 1, 0);
+  for (int l = 0; l < fp.nlevels; ++l) {
+    mt_lev[l] = (int)mt.size();
+    std::vector<std::pair<int64_t, int4>> lt;  // (bytes, {g, tile, -, -})
+    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+      const int g = fp.level_sn[k];
+      if (small[g]) {
+        int64_t by = 0;
+        for (int t : sn_tiles[g]) by += tile_bytes(t);
+        lt.push_back({by, make_int4(g, -1, 0, 0)});
+      } else {
+        for (int t : sn_tiles[g]) lt.push_back({tile_bytes(t), make_int4(g, t, 0, 0)});
+      }
+    }
+    std::stable_sort(lt.begin(), lt.end(), [](const std::pair<int64_t, int4>& x,
+                                              const std::pair<int64_t, int4>& y) { return x.first > y.first; });
+    for (auto& e : lt) {
+      int4 m = e.second;
+      m.z = (int)td.size();
+      std::vector<int> ts = m.y < 0 ? sn_tiles[m.x] : std::vector<int>{m.y};
+      for (int t : ts)
+        td.push_back(make_int4(t, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
+      m.w = (int)td.size();
+      mt.push_back(m);
+    }
+  }
+  mt_lev[fp.nlevels] = (int)mt.size();
+  int nm = 0;
+  for (int l = 0; l < fp.nlevels; ++l) {
+    ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
+    ph.push_back(make_int4(dev::PH_MF, mt_lev[l], mt_lev[l + 1], nm++));
+  }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
-    for (int g : big_at[l])
-      for (int t : sn_tiles[g]) add_task(make_int4(1, t, 0, 0), std::vector<int>{t});
-    for (int c : cl_at[l]) {
-      std::vector<int> ts;
-      for (auto it2 = clusters[c].members.rbegin(); it2 != clusters[c].members.rend(); ++it2)
-        ts.insert(ts.end(), sn_tiles[*it2].begin(), sn_tiles[*it2].end());
-      int ncbs = 0;
-      for (int g : clusters[c].members) ncbs += vncb[g];
-      add_task(make_int4(5, clusters[c].root, clusters[c].wait, ncbs), ts);
-    }
+    ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
+    ph.push_back(make_int4(dev::PH_MB, mt_lev[l], mt_lev[l + 1], nm++));
   }
-  ntasks_noprolong = (int)tk.size();
+  nphases_noprolong = (int)ph.size();
   if (prolong_n > 0) {
-    for (int e0 = 0; e0 < prolong_n; e0 += kProlongChunk)
-      add_task(make_int4(2, 0, e0, std::min(prolong_n, e0 + kProlongChunk)), none);
+    ph.push_back(make_int4(dev::PH_PR, 0, prolong_n, 0));
     pro_ptr = pro_ptr_dev;
     pro_pos = pro_pos_dev;
+    n_out = prolong_n;
   }
-  ntasks = (int)tk.size();
-  tasks.upload(tk);
-  tt_ptr.upload(ttp);
-  {
-    std::vector<int4> td(ttl.size());
-    for (size_t k = 0; k < ttl.size(); ++k) {
-      const int t = ttl[k];
-      const int4 q = tl[t];
-      const int g = q.x;
-      const int nr = fp.sn_ncol[g] + fp.sn_noff[g], nc = fp.sn_ncol[g];
-      const int rows = std::min(vRB[g], nr - q.y * vRB[g]), cols = std::min(vCB[g], nc - q.z * vCB[g]);
-      const int bytes = (int)((((int64_t)rows * cols + 1) & ~1LL) * (int64_t)sizeof(double));
-      td[k] = make_int4(t, bytes, (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32));
-    }
-    tdesc.upload(td);
-  }
+  nphases = (int)ph.size();
+  MDD_REQUIRE(nrows < INT32_MAX, 5, "sweep row space too large for 32-bit phase bounds");
+  phases.upload(ph);
+  mtask.upload(mt);
+  tdesc.upload(td);
   tiles.upload(tl);
   tile_off.upload(toff);
   sn_RB.upload(vRB); sn_CB.upload(vCB); sn_nrb.upload(vnrb); sn_ncb.upload(vncb);
   sn_rbc.upload(vrbc); sn_cbc.upload(vcbc);
-  sn_fpart.upload(vfp); sn_bpart.upload(vbp); sn_tg.upload(vtg);
+  sn_fpart.upload(vfp); sn_bpart.upload(vbp);
+  vb_off.upload(vvo);
+  gsrc.upload(vgsrc);
+  cptr.upload(vcptr);
+  cidx.upload(vcidx.empty() ? std::vector<int64_t>{0} : vcidx);
+  wsrc.upload(vwsrc);
+  vb.alloc(std::max<int64_t>(nrows, 1));
   fpart.alloc(std::max<int64_t>(nfp, 1));
   bpart.alloc(std::max<int64_t>(nbp, 1));
-  tg.alloc(std::max<int64_t>(ntg, 1));
   rb_cnt.alloc(std::max(nrbc, 1));
   cb_cnt.alloc(std::max(ncbc, 1));
-  asm_cnt.alloc(std::max(nsn, 1));
-  fwd_cnt.alloc(std::max(nsn, 1));
-  bwd_cnt.alloc(std::max(nsn, 1));
+  ticket.alloc(std::max(nm, 1));
   ctl.alloc(dev::SW_COUNT);
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
-  if (getenv("MDD_SWEEP_TRACE")) {
-    trace.alloc((size_t)4 * ntasks);
-    CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
-  }
-  if (getenv("MDD_SWEEP_STATS")) {
-    stats.alloc(10);
-    CUDA_CHECK(cudaMemset(stats.p, 0, 10 * sizeof(unsigned long long)));
-  }
-  if (getenv("MDD_PLAN_STATS")) {
-    int nbig = 0;
-    for (int g = 0; g < nsn; ++g) nbig += !single[g];
-    fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) tasks %d "
-            "clusters %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(), ntiles,
-            100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), ntasks, (int)clusters.size());
-    for (int l = 0; l < fp.nlevels; ++l) {
-      long long ent = 0, emax = 0;
-      int ncmax = 0, nrmax = 0, tcount = 0, big = 0;
-      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-        const int g = fp.level_sn[k];
-        const long long nc = fp.sn_ncol[g], no = fp.sn_noff[g];
-        const long long e = nc * (nc + 1) / 2 + nc * no;
-        ent += e;
-        emax = std::max(emax, e);
-        ncmax = std::max(ncmax, (int)nc);
-        nrmax = std::max(nrmax, (int)(nc + no));
-        tcount += (int)sn_tiles[g].size();
-        big += !single[g];
-      }
-      fprintf(stderr, "  level %2d: sn %6d (big %4d) entries %10lld max %8lld ncmax %5d nrmax %5d tiles %6d\n", l,
-              fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, emax, ncmax, nrmax, tcount);
-    }
-  }
   const int smem = dev::kSweepSmemDoubles * (int)sizeof(double);
   CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int dev_id = 0, nsm = 0, per_sm = 0;
@@ -259,10 +216,34 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
   MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
   sweep_grid = nsm * per_sm;
+  if (getenv("MDD_SWEEP_TRACE")) {
+    trace.alloc((size_t)2 * nphases * sweep_grid);
+    CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
+  }
+  if (getenv("MDD_PLAN_STATS")) {
+    int nbig = 0;
+    for (int g = 0; g < nsn; ++g) nbig += !small[g];
+    fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) mtasks %d "
+            "rows %lld contrib %lld grid %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(),
+            ntiles, 100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), (int)mt.size(),
+            (long long)nrows, (long long)vcidx.size(), sweep_grid);
+    for (int l = 0; l < fp.nlevels; ++l) {
+      long long ent = 0;
+      int big = 0;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        ent += (long long)fp.sn_ncol[g] * (fp.sn_ncol[g] + fp.sn_noff[g]);
+        big += !small[g];
+      }
+      fprintf(stderr, "  level %2d: sn %6d (big %4d) stored %10lld rows %8lld mtasks %6d\n", l,
+              fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, (long long)(lev_row[l + 1] - lev_row[l]),
+              mt_lev[l + 1] - mt_lev[l]);
+    }
+  }
 }
 
 void DevFactor::reset_counters(cudaStream_t s) {
-  for (DBuf<unsigned long long>* c : {&fwd_cnt, &bwd_cnt, &rb_cnt, &cb_cnt, &asm_cnt})
+  for (DBuf<unsigned long long>* c : {&rb_cnt, &cb_cnt, &ticket})
     CUDA_CHECK(cudaMemsetAsync(c->p, 0, c->n * sizeof(unsigned long long), s));
   std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
   c0[dev::SW_T0] = ~0ull;
@@ -274,33 +255,35 @@ dev::SweepDev DevFactor::sweep_dev() const {
   dev::SweepDev S;
   S.P = plan();
   S.dinv = dinv.p;
-  S.tasks = tasks.p;
-  S.tt_ptr = tt_ptr.p;
+  S.phases = phases.p;
+  S.nphases = nphases;
+  S.ticket = ticket.p;
+  S.mtask = mtask.p;
   S.tdesc = tdesc.p;
-  S.ntasks = ntasks;
-  S.total_bwd = total_bwd;
-  S.parent = parent.p;
   S.tiles = tiles.p;
   S.tile_off = tile_off.p;
   S.Lt = Lt.p;
   S.sn_RB = sn_RB.p; S.sn_CB = sn_CB.p; S.sn_nrb = sn_nrb.p; S.sn_ncb = sn_ncb.p;
-  S.sn_fpart = sn_fpart.p; S.sn_bpart = sn_bpart.p; S.sn_tg = sn_tg.p;
+  S.sn_fpart = sn_fpart.p; S.sn_bpart = sn_bpart.p;
   S.sn_rbc = sn_rbc.p; S.sn_cbc = sn_cbc.p;
-  S.fpart = fpart.p; S.bpart = bpart.p; S.tg = tg.p;
-  S.rb_cnt = rb_cnt.p; S.cb_cnt = cb_cnt.p; S.asm_cnt = asm_cnt.p;
-  S.fwd_cnt = fwd_cnt.p;
-  S.bwd_cnt = bwd_cnt.p;
+  S.fpart = fpart.p; S.bpart = bpart.p;
+  S.rb_cnt = rb_cnt.p; S.cb_cnt = cb_cnt.p;
+  S.vb = vb.p;
+  S.vb_off = vb_off.p;
+  S.gsrc = gsrc.p;
+  S.cptr = cptr.p;
+  S.cidx = cidx.p;
+  S.wsrc = wsrc.p;
   S.ctl = ctl.p;
   S.upd = upd.p;
   S.xf = xf.p;
   S.xb = xb.p;
   S.b = nullptr;
-  S.gmap = nullptr;
   S.pro_ptr = pro_ptr;
   S.pro_pos = pro_pos;
   S.out = nullptr;
+  S.n_out = n_out;
   S.stop = nullptr;
-  S.stats = stats.p;
   S.trace = trace.p;
   return S;
 }
@@ -308,25 +291,18 @@ dev::SweepDev DevFactor::sweep_dev() const {
 DevFactor::~DevFactor() {
   if (trace.p && getenv("MDD_SWEEP_TRACE") && !name.empty()) {
     std::vector<unsigned long long> v(trace.n);
-    std::vector<int4> tk(ntasks);
+    std::vector<int4> phh(nphases);
     if (cudaMemcpy(v.data(), trace.p, v.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
-        cudaMemcpy(tk.data(), tasks.p, tk.size() * sizeof(int4), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        cudaMemcpy(phh.data(), phases.p, phh.size() * sizeof(int4), cudaMemcpyDeviceToHost) == cudaSuccess) {
       std::string path = std::string(getenv("MDD_SWEEP_TRACE")) + "/trace_" + name + ".bin";
       if (FILE* f = fopen(path.c_str(), "wb")) {
-        int nt = ntasks;
-        fwrite(&nt, sizeof(int), 1, f);
-        fwrite(tk.data(), sizeof(int4), tk.size(), f);
+        int hdr[2] = {nphases, sweep_grid};
+        fwrite(hdr, sizeof(int), 2, f);
+        fwrite(phh.data(), sizeof(int4), phh.size(), f);
         fwrite(v.data(), 8, v.size(), f);
         fclose(f);
       }
     }
-  }
-  if (stats.p) {
-    unsigned long long v[10];
-    if (cudaMemcpy(v, stats.p, sizeof(v), cudaMemcpyDeviceToHost) == cudaSuccess)
-      fprintf(stderr, "[mdd sweep stats %s] cycles: fwd wait %llu work %llu | bwd wait %llu work %llu | "
-              "prolong wait %llu work %llu | assemble wait %llu work %llu | ticket %llu | tasks %llu\n",
-              name.c_str(), v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
   }
 }
 
@@ -338,16 +314,13 @@ void DevFactor::sweep_timing(unsigned long long* ns, unsigned long long* cnt, cu
   *cnt = v[dev::SW_TCNT];
 }
 
-void DevFactor::sweep(const double* b, const int32_t* gmap, double* out, cudaStream_t s,
-                      const int* stop) const {
+void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* stop) const {
   dev::SweepDev S = sweep_dev();
-  S.ntasks = out ? ntasks : ntasks_noprolong;
+  S.nphases = out ? nphases : nphases_noprolong;
   S.b = b;
-  S.gmap = gmap;
   S.out = out;
   S.stop = stop;
-  const int grid = std::max(1, std::min(sweep_grid, S.ntasks));
-  dev::k_sweep<<<grid, dev::kSweepThreads, dev::kSweepSmemDoubles * sizeof(double), s>>>(S);
+  dev::k_sweep<<<sweep_grid, dev::kSweepThreads, dev::kSweepSmemDoubles * sizeof(double), s>>>(S);
 }
 
 void DevFactor::check_abort(cudaStream_t s) {
@@ -356,7 +329,7 @@ void DevFactor::check_abort(cudaStream_t s) {
   CUDA_CHECK(cudaStreamSynchronize(s));
   if (ab) {
     reset_counters(s);
-    throw Error(5, "supernodal sweep aborted (dependency wait timed out)");
+    throw Error(5, "supernodal sweep aborted (barrier wait timed out)");
   }
 }
 

@@ -89,29 +89,24 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
                                   double tol, uint8_t* __restrict__ dropped, int* __restrict__ err);
 
 // -------------------------------------------- supernodal triangular sweeps
-// (sweep.cu) control words of a persistent sweep
-enum { SW_TICKET = 0, SW_EXIT, SW_EPOCH, SW_BWD_DONE, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
+// (sweep.cu) control words of a persistent sweep and its phase kinds
+enum { SW_EPOCH = 0, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
+enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR };
 constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 4096;   // doubles per tile (32 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
-constexpr int64_t kClusterMax = 32768;  // stored entries of a subtree swept by one task
 constexpr int kSweepSmemDoubles = 2 * kTileMax + 2 * kVecMax + kSweepThreads;
 
 struct SweepDev {
   PlanDev P;
   const double* dinv;
-  // tasks {type, a, b, c}: 0 fwd tile (a = tile) / 1 bwd tile / 2 prolong [b, c) /
-  // 3 assemble (a = supernode) / 4 cluster fwd (a = cluster root, b = wait for its
-  // children) / 5 cluster bwd (a = cluster root); tiles streamed by a task:
-  // task_tiles[tt_ptr[t] .. tt_ptr[t+1])
-  const int4* tasks;
-  const int* tt_ptr;
-  const int4* tdesc;             // per task-ordered tile: {tile, bytes, offset lo, offset hi}
-  int ntasks;
-  int total_bwd;                 // backward column blocks per launch
-  const int* parent;             // supernode parent (-1 root)
-  // tiles
+  // phases {kind, a, b, ticket slot}: G: rows [a, b) of vb; M: mtask [a, b); PR
+  const int4* phases;
+  int nphases;
+  unsigned long long* ticket;    // one cumulative ticket counter per M phase
+  const int4* mtask;             // {supernode, tile (-1: small supernode), tdesc [first, end)}
+  const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
   const int64_t* tile_off;       // into Lt
   const double* Lt;              // tiled P-form panels
@@ -119,31 +114,32 @@ struct SweepDev {
   const int* sn_CB;
   const int* sn_nrb;
   const int* sn_ncb;
-  const int64_t* sn_fpart;       // big supernodes: partial sums / rhs offsets
+  const int64_t* sn_fpart;       // big supernodes: partial-sum offsets
   const int64_t* sn_bpart;
-  const int64_t* sn_tg;
   const int* sn_rbc;             // offsets of the row-block / column-block counters
   const int* sn_cbc;
   double* fpart;
   double* bpart;
-  double* tg;
   unsigned long long* rb_cnt;
   unsigned long long* cb_cnt;
-  unsigned long long* asm_cnt;
-  unsigned long long* fwd_cnt;   // row blocks finished (cumulative)
-  unsigned long long* bwd_cnt;   // column blocks finished (cumulative)
+  // per-supernode row vectors (t forward, w backward): rows of g at vb_off[g]
+  double* vb;
+  const int64_t* vb_off;
+  const int32_t* gsrc;           // row -> index into b (column rows) or -1
+  const int64_t* cptr;           // row -> children update entries (into upd)
+  const int64_t* cidx;
+  const int64_t* wsrc;           // row -> xf index (>= 0) or -(xb index) - 1
   unsigned long long* ctl;       // SW_* words
   double* upd;                   // update vectors (noff per supernode)
   double* xf;                    // forward result z (positions)
   double* xb;                    // solution (positions)
-  const double* b;               // right-hand side: b[gmap[pos]] or b[pos]
-  const int32_t* gmap;
+  const double* b;               // right-hand side (global index space of gsrc)
   const int64_t* pro_ptr;        // prolongation (global dof -> positions)
   const int32_t* pro_pos;
   double* out;                   // prolongation target (global)
+  int n_out;
   const int* stop;               // PCG stop flag (nullable): set -> no-op launch
-  unsigned long long* stats;     // optional cycle accounting (MDD_SWEEP_STATS=1)
-  unsigned long long* trace;     // optional per-task timeline (MDD_SWEEP_TRACE=dir)
+  unsigned long long* trace;     // optional per-phase timeline (MDD_SWEEP_TRACE=dir)
 };
 __global__ void k_sweep(SweepDev S);
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,

@@ -1,36 +1,34 @@
-// Persistent, dependency-driven supernodal triangular sweep (sm_100a, FP64).
+// Persistent, level-synchronous supernodal triangular sweep (sm_100a, FP64).
 //
 // One launch applies A_i^{-1} for ALL subdomains at once (north_star: "local
 // solves A_i^{-1} as supernodal sparse LDL^T factors applied by hand-written
 // level-scheduled triangular-solve kernels, with dense supernode blocks as
-// warp-tiled TRSV"), fusing the restriction R_i (gather in the leaves), the
-// forward sweep L y = b, the diagonal D^{-1}, the backward sweep L^T x = z and
-// the prolongation sum_i R_i^T x_i (PAPER.md eq. AS, M_AS = sum R_i^T A_i^{-1} R_i).
-// The same kernel applies E^{-1} for the coarse correction.
+// warp-tiled TRSV"), fusing the restriction R_i, the forward sweep L y = b, the
+// diagonal D^{-1}, the backward sweep L^T x = z and the prolongation
+// sum_i R_i^T x_i (PAPER.md eq. AS: M_AS = sum_i R_i^T A_i^{-1} R_i).  The same
+// kernel applies E^{-1} for the coarse correction Z E^{-1} Z^T.
 //
-// Panels are in "partitioned-inverse" form P = [L11^{-1}; L21 L11^{-1}], so
+// Panels are in "partitioned-inverse" form P = [L11^{-1}; L21 L11^{-1}], so per
+// supernode
 //   forward :  z_c = D^{-1} (L11^{-1} t_c),     u = t_off - (L21 L11^{-1}) t_c
 //   backward:  x_c = L11^{-T} z_c - (L21 L11^{-1})^T x_off
-// are plain dense mat-vecs.  Every panel is cut into tiles of <= kTileMax
-// doubles stored contiguously (factor_driver.cu), so each task streams ONE
-// contiguous block from HBM with a single TMA bulk copy (cp.async.bulk +
-// mbarrier) into shared memory.  The copy for the next task is issued before the
-// current task waits for its dependencies, so HBM latency, ticket latency and
-// dependency latency overlap.
+// are plain dense mat-vecs over contiguous tiles (<= kTileMax doubles), each
+// streamed from HBM by ONE TMA bulk copy (cp.async.bulk + mbarrier) with one
+// task of look-ahead.
 //
-// A small supernode (nr <= kVecMax, nr*nc <= kTileMax) is one tile and one task
-// per direction.  A big one has an assemble task (its right-hand side t = b +
-// children updates, to global memory) and RB x CB tiles whose partial sums are
-// combined, in a fixed order (bit-reproducible), by the last tile to arrive in
-// each row block (forward) or column block (backward).
-//
-// Scheduling: tasks (forward work in level order, backward work in reverse level
-// order, prolongation chunks) are handed out by an atomic ticket; a task only
-// waits for tasks with smaller tickets, so the schedule is deadlock-free for any
-// grid size (also with one ticket of look-ahead).  Counters are cumulative
-// across launches (epoch = launches so far); the last CTA to exit advances the
-// epoch.  A wait that exceeds kSpinTimeoutNs raises an abort flag (reported by
-// the host) instead of hanging the device.
+// The launch walks a fixed list of phases separated by grid barriers (all CTAs
+// are co-resident: one persistent CTA set sized by the occupancy calculator):
+//   for each level, leaves first:   G_f  (flat gather of every supernode's
+//     right-hand side t = [b_c ; 0] + children's update vectors, a precomputed
+//     row -> contributions list, so no scatter and no atomics)  |  M_f (tiles)
+//   for each level, root first:     G_b  (w = [z_c ; -x_off])  |  M_b (tiles)
+//   prolongation.
+// Within M phases CTAs take tasks from an atomic ticket (largest first).  A task
+// is either a small supernode (all its column tiles, accumulated in shared
+// memory by one CTA) or one RB x CB tile of a big supernode, whose partial sums
+// the last tile to arrive combines in a fixed order -- every reduction is
+// bit-reproducible.  Counters are cumulative across launches (epoch); a barrier
+// wait that exceeds kSpinTimeoutNs raises an abort flag reported by the host.
 #include "kernels.cuh"
 
 namespace mdd {
@@ -78,61 +76,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       : "memory");
 }
 
-// one thread: spin until *p >= target; false on abort / timeout
-__device__ bool wait_ge(const unsigned long long* p, unsigned long long target, unsigned long long* ctl) {
-  if (ld_acquire(p) >= target) return true;
-  const unsigned long long t0 = globaltimer();
-  unsigned int ns = 32;
-  for (int it = 0;; ++it) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
-    if (ld_acquire(p) >= target) return true;
-    if ((it & 63) == 63) {
-      if (*(volatile unsigned long long*)&ctl[SW_ABORT]) return false;
-      if (globaltimer() - t0 > kSpinTimeoutNs) {
-        atomicExch(&ctl[SW_ABORT], 1ull);
-        return false;
+// grid-wide barrier over co-resident CTAs (cumulative counter, no reset)
+__device__ void grid_barrier(unsigned long long* ctl, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&ctl[SW_BAR], 1ull);
+    if (ld_acquire(&ctl[SW_BAR]) < target) {
+      const unsigned long long t0 = globaltimer();
+      for (int it = 0;; ++it) {
+        __nanosleep(64);
+        if (ld_acquire(&ctl[SW_BAR]) >= target) break;
+        if ((it & 255) == 255) {
+          if (*(volatile unsigned long long*)&ctl[SW_ABORT]) break;
+          if (globaltimer() - t0 > kSpinTimeoutNs) {
+            atomicExch(&ctl[SW_ABORT], 1ull);
+            break;
+          }
+        }
       }
     }
-  }
-}
-
-// warp 0: wait until every child of g finished its forward work (lanes check the
-// children in parallel); the verdict is returned to all threads
-__device__ bool wait_children(const SweepDev& S, int g, unsigned long long cur, int* s_flag) {
-  const int tid = threadIdx.x;
-  if (tid < 32) {
-    bool ok = *(volatile unsigned long long*)&S.ctl[SW_ABORT] == 0;
-    const i64 c0 = S.P.child_ptr[g], c1 = S.P.child_ptr[g + 1];
-    for (i64 ci = c0 + tid; ok && ci < c1; ci += 32) {
-      const int c = S.P.child_list[ci];
-      ok = wait_ge(&S.fwd_cnt[c], cur * (unsigned long long)S.sn_nrb[c], S.ctl);
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    if (tid == 0) {
-      __threadfence();
-      *s_flag = ok;
-    }
-  }
-  __syncthreads();
-  return *s_flag != 0;
-}
-
-__device__ bool wait_one(const unsigned long long* p, unsigned long long target,
-                         unsigned long long* ctl, int* s_flag) {
-  if (threadIdx.x == 0) {
-    bool ok = *(volatile unsigned long long*)&ctl[SW_ABORT] == 0;
-    if (ok) ok = wait_ge(p, target, ctl);
     __threadfence();
-    *s_flag = ok;
   }
   __syncthreads();
-  return *s_flag != 0;
-}
-
-__device__ __forceinline__ void signal_add(unsigned long long* p) {
-  __threadfence();
-  atomicAdd(p, 1ull);
 }
 
 struct TileGeo {
@@ -223,310 +189,181 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   const PlanDev& P = S.P;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
+  const unsigned long long grid = gridDim.x;
   if (tid == 0) {
     atomicMin(&S.ctl[SW_T0], globaltimer());
     mbar_init(&mbar[0]);
     mbar_init(&mbar[1]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  long long st_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long c_prev = clock64();
-#define STAT_MARK(slot) \
-  if (S.stats && tid == 0) { long long c_ = clock64(); st_acc[(slot)] += c_ - c_prev; c_prev = c_; } \
-  if (S.trace && tid == 0 && ((slot) == 0 || (slot) == 2 || (slot) == 4 || (slot) == 6)) \
-    S.trace[4 * (size_t)t + 1] = globaltimer();
-
-  // thread 0 helpers: start streaming a tile into a stage buffer.  tdesc[k] =
-  // {tile, bytes, offset lo, offset hi} in task order: one load per prefetch
-  auto prefetch_k = [&](int k, int b) {
-    const int4 d = S.tdesc[k];
-    const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
-    bulk_load(sm + b * kTileMax, S.Lt + off, (uint32_t)d.y, &mbar[b]);
-  };
-  auto first_k = [&](int t) -> int {
-    if (t >= S.ntasks) return -1;
-    const int a = S.tt_ptr[t];
-    return a < S.tt_ptr[t + 1] ? a : -1;
-  };
-  int tn = 0;  // thread 0: the look-ahead ticket
-  if (tid == 0) {
-    const int t0 = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
-    s_next[0] = t0;
-    const int fk = first_k(t0);
-    if (fk >= 0) prefetch_k(fk, 0);
-  }
   __syncthreads();
-  uint32_t par[2] = {0u, 0u};
-  int it = 0, buf = 0;
-  // wait for the tile in `buf` and issue the next one of the stream into buf ^ 1
-  auto next_tile_and_wait = [&](int k, int kend) {
-    if (tid == 0) {
-      const int nk = k + 1 < kend ? k + 1 : first_k(tn);
-      if (nk >= 0) prefetch_k(nk, buf ^ 1);
-    }
-    mbar_wait(&mbar[buf], par[buf]);
-    par[buf] ^= 1u;
-  };
-  for (;;) {
-    const int t = s_next[it & 1];
-    if (t >= S.ntasks) break;
-    const int4 tk = S.tasks[t];
-    const int type = tk.x;
-    const int ka = S.tt_ptr[t], kb = S.tt_ptr[t + 1];
-    if (tid == 0) {
-      tn = (int)atomicAdd(&S.ctl[SW_TICKET], 1ull);
-      s_next[(it + 1) & 1] = tn;
-      if (ka == kb) {  // no tile of ours in flight: the next task's first tile goes to buf
-        const int fk = first_k(tn);
-        if (fk >= 0) prefetch_k(fk, buf);
-      }
-    }
-    STAT_MARK(8);
-    if (S.trace && tid == 0) {
-      S.trace[4 * (size_t)t] = globaltimer();
-      S.trace[4 * (size_t)t + 3] = ((unsigned long long)blockIdx.x << 8) | (unsigned long long)type;
-    }
-    double* const T = sm + buf * kTileMax;
+  uint32_t par0 = 0u, par1 = 0u;
+  int buf = 0;
+  const size_t gthreads = (size_t)gridDim.x * kSweepThreads;
+  const size_t gtid = (size_t)blockIdx.x * kSweepThreads + tid;
 
-    if (type == 0) {
-      // ============================================ forward tile of a big supernode
-      const int4 tl = S.tiles[tk.y];
-      const int g = tl.x, rb = tl.y, cb = tl.z;
-      const TileGeo G = geo(S, g, rb, cb);
-      const i64 col0 = P.sn_col0[g];
-      const bool ok = wait_one(&S.asm_cnt[g], cur, S.ctl, &s_flag);
-      STAT_MARK(0);
-      if (ok) {
-        const double* tg = S.tg + S.sn_tg[g] + cb * G.CB;
-        for (int k = tid; k < G.cols; k += kSweepThreads) vec[k] = __ldcg(tg + k);
-        __syncthreads();
+  for (int ph = 0; ph < S.nphases; ++ph) {
+    const int4 PH = S.phases[ph];
+    const int kind = PH.x;
+    const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
+    if (kind == PH_GF) {
+      // t = [b_c ; 0] + children's updates, one row per thread
+      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) {
+        const int src = S.gsrc[q];
+        double v = src >= 0 ? __ldg(S.b + src) : 0.0;
+        for (i64 k = S.cptr[q]; k < S.cptr[q + 1]; ++k) v += __ldcg(S.upd + S.cidx[k]);
+        S.vb[q] = v;
       }
-      next_tile_and_wait(ka, kb);
-      if (ok) {
-        double* fp = S.fpart + S.sn_fpart[g] + (i64)cb * G.nr + (i64)rb * G.RB;
-        tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) { fp[i] = y; });
-        __syncthreads();
-        const int rend = min(G.nr, (rb + 1) * G.RB);
-        const int ntl = min(G.ncb, (rend + G.CB - 1) / G.CB);
+    } else if (kind == PH_GB) {
+      // w = [z_c ; -x_off]
+      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) {
+        const i64 w = S.wsrc[q];
+        S.vb[q] = w >= 0 ? __ldcg(S.xf + w) : -__ldcg(S.xb + (-w - 1));
+      }
+    } else if (kind == PH_PR) {
+      for (size_t e = gtid; e < (size_t)S.n_out; e += gthreads) {
+        double s = 0.0;
+        for (i64 k = S.pro_ptr[e]; k < S.pro_ptr[e + 1]; ++k) s += __ldcg(S.xb + S.pro_pos[k]);
+        S.out[e] = s;
+      }
+    } else if (!*(volatile unsigned long long*)&S.ctl[SW_ABORT]) {
+      // ---------------------------------------------- M phase: tiles
+      const bool fwd = kind == PH_MF;
+      const int ta = PH.y, ntk = PH.z - PH.y;
+      const unsigned long long base = (cur - 1) * ((unsigned long long)ntk + grid);
+      unsigned long long* tick = &S.ticket[PH.w];
+      auto prefetch_k = [&](int k, int b) {
+        const int4 d = S.tdesc[k];
+        const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
+        bulk_load(sm + b * kTileMax, S.Lt + off, (uint32_t)d.y, &mbar[b]);
+      };
+      int tn = 0;
+      if (tid == 0) {
+        const int k0 = (int)(atomicAdd(tick, 1ull) - base);
+        s_next[0] = k0;
+        if (k0 < ntk) prefetch_k(S.mtask[ta + k0].z, buf);
+      }
+      __syncthreads();
+      for (int it = 0;; ++it) {
+        const int k = s_next[it & 1];
+        if (k >= ntk) break;
+        const int4 mt = S.mtask[ta + k];  // {supernode, tile (-1: small), first tdesc, end tdesc}
         if (tid == 0) {
-          __threadfence();
-          const unsigned long long old = atomicAdd(&S.rb_cnt[S.sn_rbc[g] + rb], 1ull);
-          s_flag = (old + 1 == cur * (unsigned long long)ntl);
-          __threadfence();
+          tn = (int)(atomicAdd(tick, 1ull) - base);
+          s_next[(it + 1) & 1] = tn;
         }
-        __syncthreads();
-        if (s_flag) {
-          // last tile of the row block: combine partial sums in column-block order
-          const double* fb = S.fpart + S.sn_fpart[g] + (i64)rb * G.RB;
-          const double* tg = S.tg + S.sn_tg[g] + (i64)rb * G.RB;
-          for (int i = tid; i < G.rows; i += kSweepThreads) {
-            double s = 0.0;
-            for (int q = 0; q < ntl; ++q) s += __ldcg(fb + (i64)q * G.nr + i);
-            const int r = rb * G.RB + i;
-            if (r < G.nc) S.xf[col0 + r] = __ldg(S.dinv + col0 + r) * s;
-            else S.upd[P.sn_uptr[g] + (r - G.nc)] = __ldcg(tg + i) - s;
-          }
-          __syncthreads();
-          if (tid == 0) signal_add(&S.fwd_cnt[g]);
-        }
-      }
-      buf ^= 1;
-      STAT_MARK(1);
-    } else if (type == 1) {
-      // ============================================ backward tile of a big supernode
-      const int4 tl = S.tiles[tk.y];
-      const int g = tl.x, rb = tl.y, cb = tl.z;
-      const TileGeo G = geo(S, g, rb, cb);
-      const i64 col0 = P.sn_col0[g];
-      const int p = S.parent[g];
-      const bool ok = p >= 0 ? wait_one(&S.bwd_cnt[p], cur * (unsigned long long)S.sn_ncb[p], S.ctl, &s_flag)
-                             : wait_one(&S.fwd_cnt[g], cur * (unsigned long long)G.nrb, S.ctl, &s_flag);
-      STAT_MARK(2);
-      if (ok) {
-        const i64* rows = P.offrows + P.sn_rowptr[g];
-        for (int i = tid; i < G.rows; i += kSweepThreads) {
-          const int r = rb * G.RB + i;
-          vec[i] = r < G.nc ? __ldcg(S.xf + col0 + r) : -__ldcg(S.xb + rows[r - G.nc]);
-        }
-        __syncthreads();
-      }
-      next_tile_and_wait(ka, kb);
-      if (ok) {
-        double* bp = S.bpart + S.sn_bpart[g] + (i64)rb * G.nc + (i64)cb * G.CB;
-        tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { bp[j] = y; });
-        __syncthreads();
-        const int rb0 = (cb * G.CB) / G.RB;
-        if (tid == 0) {
-          __threadfence();
-          const unsigned long long old = atomicAdd(&S.cb_cnt[S.sn_cbc[g] + cb], 1ull);
-          s_flag = (old + 1 == cur * (unsigned long long)(G.nrb - rb0));
-          __threadfence();
-        }
-        __syncthreads();
-        if (s_flag) {
-          // last tile of the column block: combine partial sums in row-block order
-          const double* bb = S.bpart + S.sn_bpart[g] + (i64)cb * G.CB;
-          for (int j = tid; j < G.cols; j += kSweepThreads) {
-            double s = 0.0;
-            for (int q = rb0; q < G.nrb; ++q) s += __ldcg(bb + (i64)q * G.nc + j);
-            S.xb[col0 + cb * G.CB + j] = s;
-          }
-          __syncthreads();
-          if (tid == 0) {
-            signal_add(&S.bwd_cnt[g]);
-            atomicAdd(&S.ctl[SW_BWD_DONE], 1ull);
-          }
-        }
-      }
-      buf ^= 1;
-      STAT_MARK(3);
-    } else if (type == 4) {
-      // ============================================ forward of a cluster of small
-      // supernodes (a subtree, or one supernode whose children were waited for),
-      // postorder, one CTA: no inter-CTA synchronisation inside the cluster
-      bool ok = true;
-      if (tk.z) ok = wait_children(S, tk.y, cur, &s_flag);
-      else if (tid == 0 && *(volatile unsigned long long*)&S.ctl[SW_ABORT]) ok = false;
-      STAT_MARK(0);
-      for (int k = ka; k < kb; ++k) {
-        const int4 tl = S.tiles[S.tdesc[k].x];
-        const int g = tl.x, cb = tl.z;
-        const TileGeo G = geo(S, g, 0, cb);
+        const int g = mt.x;
         const i64 col0 = P.sn_col0[g];
-        if (cb == 0 && ok) {
-          // t = [b_c ; 0] + extend-add of the children's update vectors; acc = 0
-          for (int q = tid; q < G.nr; q += kSweepThreads) {
-            vec[q] = q < G.nc ? (S.gmap ? __ldg(S.b + __ldg(S.gmap + col0 + q)) : __ldg(S.b + col0 + q)) : 0.0;
+        const i64 vo = S.vb_off[g];
+        // wait for the tile in `buf`; stream the next one (this task's or the next
+        // task's first) into buf ^ 1
+        auto next_tile_and_wait = [&](int kk) {
+          if (tid == 0) {
+            const int nk = kk + 1 < mt.w ? kk + 1 : (tn < ntk ? S.mtask[ta + tn].z : -1);
+            if (nk >= 0) prefetch_k(nk, buf ^ 1);
+          }
+          if (buf) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
+          else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
+        };
+        if (mt.y < 0) {
+          // ---------------- small supernode: all column tiles, one CTA
+          const TileGeo G0 = geo(S, g, 0, 0);
+          for (int q = tid; q < G0.nr; q += kSweepThreads) {
+            vec[q] = __ldcg(S.vb + vo + q);
             vec2[q] = 0.0;
           }
           __syncthreads();
-          for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
-            const int c = P.child_list[ci];
-            const int noc = P.sn_noff[c];
-            const double* u = S.upd + P.sn_uptr[c];
-            const int* rm = P.relmap + P.sn_rowptr[c];
-            for (int a = tid; a < noc; a += kSweepThreads) vec[rm[a]] += __ldcg(u + a);
-            __syncthreads();
-          }
-        }
-        next_tile_and_wait(k, kb);
-        if (ok) {
-          const double* v = vec + cb * G.CB;
-          tile_matvec(sm + buf * kTileMax, G.rows, G.cols, v, red,
-                      [&](int i, double y) { vec2[i] += y; });
-          __syncthreads();
-          if (cb == G.ncb - 1) {
-            double* const xf = S.xf + col0;
-            double* const upd = S.upd + P.sn_uptr[g];
-            for (int i = tid; i < G.nr; i += kSweepThreads) {
-              if (i < G.nc) xf[i] = __ldg(S.dinv + col0 + i) * vec2[i];
-              else upd[i - G.nc] = vec[i] - vec2[i];
+          for (int kk = mt.z; kk < mt.w; ++kk) {
+            const int cb = S.tiles[S.tdesc[kk].x].z;
+            const TileGeo G = geo(S, g, 0, cb);
+            next_tile_and_wait(kk);
+            const double* T = sm + buf * kTileMax;
+            if (fwd) {
+              tile_matvec(T, G.rows, G.cols, vec + cb * G.CB, red, [&](int i, double y) { vec2[i] += y; });
+            } else {
+              double* const xb = S.xb + col0 + cb * G.CB;
+              tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
             }
             __syncthreads();
-            // only the cluster root is waited for from outside the cluster
-            if (tid == 0 && g == tk.y) signal_add(&S.fwd_cnt[g]);
+            buf ^= 1;
           }
-        }
-        buf ^= 1;
-      }
-      STAT_MARK(1);
-    } else if (type == 5) {
-      // ============================================ backward of a cluster (reverse
-      // postorder: every ancestor inside the cluster is done before its children)
-      const int g0 = tk.y;
-      const int p0 = S.parent[g0];
-      const bool ok = p0 >= 0 ? wait_one(&S.bwd_cnt[p0], cur * (unsigned long long)S.sn_ncb[p0], S.ctl, &s_flag)
-                              : wait_one(&S.fwd_cnt[g0], cur * (unsigned long long)S.sn_nrb[g0], S.ctl, &s_flag);
-      STAT_MARK(2);
-      for (int k = ka; k < kb; ++k) {
-        const int4 tl = S.tiles[S.tdesc[k].x];
-        const int g = tl.x, cb = tl.z;
-        const TileGeo G = geo(S, g, 0, cb);
-        const i64 col0 = P.sn_col0[g];
-        if (cb == 0 && ok) {
-          const i64* rows = P.offrows + P.sn_rowptr[g];
-          for (int i = tid; i < G.nr; i += kSweepThreads)
-            vec[i] = i < G.nc ? __ldcg(S.xf + col0 + i) : -__ldcg(S.xb + rows[i - G.nc]);
+          if (fwd) {
+            double* const upd = S.upd + P.sn_uptr[g];
+            for (int i = tid; i < G0.nr; i += kSweepThreads) {
+              if (i < G0.nc) S.xf[col0 + i] = __ldg(S.dinv + col0 + i) * vec2[i];
+              else upd[i - G0.nc] = vec[i] - vec2[i];
+            }
+          }
+        } else {
+          // ---------------- one tile of a big supernode
+          const int4 tl = S.tiles[mt.y];
+          const int rb = tl.y, cb = tl.z;
+          const TileGeo G = geo(S, g, rb, cb);
+          if (fwd) {
+            for (int q = tid; q < G.cols; q += kSweepThreads) vec[q] = __ldcg(S.vb + vo + cb * G.CB + q);
+          } else {
+            for (int q = tid; q < G.rows; q += kSweepThreads) vec[q] = __ldcg(S.vb + vo + rb * G.RB + q);
+          }
           __syncthreads();
-        }
-        next_tile_and_wait(k, kb);
-        if (ok) {
-          double* const xb = S.xb + col0 + cb * G.CB;
-          tile_matvec_t(sm + buf * kTileMax, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
+          next_tile_and_wait(mt.z);
+          const double* T = sm + buf * kTileMax;
+          if (fwd) {
+            double* fp = S.fpart + S.sn_fpart[g] + (i64)cb * G.nr + (i64)rb * G.RB;
+            tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) { fp[i] = y; });
+          } else {
+            double* bp = S.bpart + S.sn_bpart[g] + (i64)rb * G.nc + (i64)cb * G.CB;
+            tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { bp[j] = y; });
+          }
           __syncthreads();
-          // children outside the cluster exist only for a single-supernode cluster
-          if (cb == G.ncb - 1 && tid == 0 && tk.z) {
+          buf ^= 1;
+          const int rend = min(G.nr, (rb + 1) * G.RB);
+          const int ntl = fwd ? min(G.ncb, (rend + G.CB - 1) / G.CB) : G.nrb - (cb * G.CB) / G.RB;
+          if (tid == 0) {
             __threadfence();
-            atomicAdd(&S.bwd_cnt[g], (unsigned long long)G.ncb);
-          }
-        }
-        buf ^= 1;
-      }
-      if (tid == 0 && ok) {
-        __threadfence();
-        atomicAdd(&S.ctl[SW_BWD_DONE], (unsigned long long)tk.w);  // column blocks of the cluster
-      }
-      STAT_MARK(3);
-    } else if (type == 3) {
-      // ============================================ assemble t of a big supernode
-      const int g = tk.y;
-      const bool ok = wait_children(S, g, cur, &s_flag);
-      STAT_MARK(6);
-      if (ok) {
-        const int nc = P.sn_ncol[g], nr = nc + P.sn_noff[g];
-        const i64 col0 = P.sn_col0[g];
-        double* tg = S.tg + S.sn_tg[g];
-        for (int k = tid; k < nr; k += kSweepThreads)
-          tg[k] = k < nc ? (S.gmap ? __ldg(S.b + __ldg(S.gmap + col0 + k)) : __ldg(S.b + col0 + k)) : 0.0;
-        __syncthreads();
-        for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
-          const int c = P.child_list[ci];
-          const int noc = P.sn_noff[c];
-          const double* u = S.upd + P.sn_uptr[c];
-          const int* rm = P.relmap + P.sn_rowptr[c];
-          for (int a = tid; a < noc; a += kSweepThreads) {
-            const int pos = rm[a];
-            tg[pos] = __ldcg(tg + pos) + __ldcg(u + a);
+            unsigned long long* c = fwd ? &S.rb_cnt[S.sn_rbc[g] + rb] : &S.cb_cnt[S.sn_cbc[g] + cb];
+            s_flag = atomicAdd(c, 1ull) + 1 == cur * (unsigned long long)ntl;
+            __threadfence();
           }
           __syncthreads();
+          if (s_flag) {
+            // last tile of its row block (fwd) / column block (bwd): fixed-order combine
+            if (fwd) {
+              const double* fb = S.fpart + S.sn_fpart[g] + (i64)rb * G.RB;
+              for (int i = tid; i < G.rows; i += kSweepThreads) {
+                double s = 0.0;
+                for (int q = 0; q < ntl; ++q) s += __ldcg(fb + (i64)q * G.nr + i);
+                const int r = rb * G.RB + i;
+                if (r < G.nc) S.xf[col0 + r] = __ldg(S.dinv + col0 + r) * s;
+                else S.upd[P.sn_uptr[g] + (r - G.nc)] = __ldcg(S.vb + vo + r) - s;
+              }
+            } else {
+              const int rb0 = (cb * G.CB) / G.RB;
+              const double* bb = S.bpart + S.sn_bpart[g] + (i64)cb * G.CB;
+              for (int j = tid; j < G.cols; j += kSweepThreads) {
+                double s = 0.0;
+                for (int q = rb0; q < G.nrb; ++q) s += __ldcg(bb + (i64)q * G.nc + j);
+                S.xb[col0 + cb * G.CB + j] = s;
+              }
+            }
+          }
         }
-        if (tid == 0) signal_add(&S.asm_cnt[g]);
+        __syncthreads();
       }
-      STAT_MARK(7);
-    } else {
-      // ============================================ prolongation chunk
-      const bool ok = wait_one(&S.ctl[SW_BWD_DONE], cur * (unsigned long long)S.total_bwd, S.ctl, &s_flag);
-      STAT_MARK(4);
-      if (ok) {
-        for (int e = tk.z + tid; e < tk.w; e += kSweepThreads) {
-          double s = 0.0;
-          for (i64 k = S.pro_ptr[e]; k < S.pro_ptr[e + 1]; ++k) s += __ldcg(S.xb + S.pro_pos[k]);
-          S.out[e] = s;
-        }
-      }
-      STAT_MARK(5);
     }
-    if (S.stats && tid == 0) st_acc[9] += 1;
-    if (S.trace && tid == 0) S.trace[4 * (size_t)t + 2] = globaltimer();
-    __syncthreads();
-    ++it;
+    if (S.trace && tid == 0) {
+      S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x)] = t_ph;
+      S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x) + 1] = globaltimer();
+    }
+    if (ph + 1 < S.nphases)
+      grid_barrier(S.ctl, ((cur - 1) * (unsigned long long)(S.nphases - 1) + ph + 1) * grid);
   }
-#undef STAT_MARK
-  if (S.stats && tid == 0)
-    for (int q = 0; q < 10; ++q) atomicAdd(&S.stats[q], (unsigned long long)st_acc[q]);
-  // exit protocol: the last CTA resets the ticket and advances the epoch
-  if (tid == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
+    // every CTA read the epoch before the first barrier
+    S.ctl[SW_TSUM] += globaltimer() - S.ctl[SW_T0];
+    S.ctl[SW_TCNT] += 1;
+    S.ctl[SW_T0] = ~0ull;
+    S.ctl[SW_EPOCH] = cur;
     __threadfence();
-    const unsigned long long prev = atomicAdd(&S.ctl[SW_EXIT], 1ull);
-    if (prev == (unsigned long long)gridDim.x - 1) {
-      S.ctl[SW_TSUM] += globaltimer() - S.ctl[SW_T0];
-      S.ctl[SW_TCNT] += 1;
-      S.ctl[SW_T0] = ~0ull;
-      S.ctl[SW_TICKET] = 0;
-      S.ctl[SW_EXIT] = 0;
-      S.ctl[SW_EPOCH] = cur;
-      __threadfence();
-    }
   }
 }
 

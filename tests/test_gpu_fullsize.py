@@ -54,9 +54,12 @@ def test_single_subdomain_local_solve(c1, sub):
     zg = z.cpu().numpy()
     # kappa(A_i) ~ 1e11 for the contrast-1e4, gamma-1e-4 recipe (R9)
     assert np.linalg.norm(zg - ref) <= 1e-4 * np.linalg.norm(ref)
-    # the residual of the local system is at round-off level
-    res = Ai @ zg[d] - r[d]
-    assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(r[d])
+    # backward stability: the residual is at the level of a direct solver's
+    # (||A_i|| ||z|| eps), here compared with SuperLU's own residual
+    res = np.linalg.norm(Ai @ zg[d] - r[d])
+    res_lu = np.linalg.norm(Ai @ zi - r[d])
+    bound = np.finfo(float).eps * spla.norm(Ai, 1) * np.linalg.norm(zi)
+    assert res <= 100 * max(res_lu, bound)
     outside = np.setdiff1d(np.arange(len(r)), d)
     assert not zg[outside].any()
 
