@@ -194,14 +194,14 @@ def main():
         assert ok, f"PCG did not converge (relres {relres})"
         iters.append(it)
 
-    # ---- timed steps (device events on the library's stream, L2 flushed between steps)
-    G.set_profiling(True)
-    prof_acc = {}
+    # ---- timed steps: the whole solve is one CUDA-graph launch (device-side WHILE
+    # loop); CUDA events on the library's stream, L2 flushed between steps
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clk = Clocks(local)
     clk.start()
+    sw0 = G.sweep_timing("local")
     t_ms = 0.0
     launches = 0
     work = 0
@@ -217,16 +217,12 @@ def main():
         t_ms += e0.elapsed_time(e1)
         launches += G.last_launches()
         work += n * it
-        for k, (ms, cnt) in G.profile().items():
-            a = prof_acc.setdefault(k, [0.0, 0])
-            a[0] += ms
-            a[1] += cnt
         iters.append(it)
     torch.cuda.synchronize()
+    sw1 = G.sweep_timing("local")
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
-    G.set_profiling(False)
     step_ms = t_ms / args.steps
     # max over ranks
     tt = torch.tensor([step_ms, float(work)], dtype=torch.float64, device="cuda")
@@ -240,6 +236,28 @@ def main():
         step_ms_max = step_ms
         total_work = float(work)
     value = total_work / (step_ms_max * args.steps / 1e3)
+    in_step = ((sw1[0] - sw0[0]) / max(1, sw1[1] - sw0[1]), sw1[1] - sw0[1])
+
+    # ---- the dominant kernel alone: the persistent sweep of the local solves
+    # (one k_sweep launch per mdd_apply_local), CUDA events on its stream
+    v = torch.randn(n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(v)
+    for _ in range(3):
+        G.apply_local(v, y)
+    reps = 20
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        G.apply_local(v, y)
+    e1.record(stream)
+    e1.synchronize()
+    sweep_ms = e0.elapsed_time(e1) / reps
+    # per-phase breakdown of one solve (eager path with events; not the timed path)
+    G.set_profiling(True)
+    G.solve(f, x, tol=TOL, maxit=args.maxit)
+    prof = G.profile()
+    G.set_profiling(False)
 
     # ---- e2e: host buffers through mdd_solve_host (H2D of f + D2H of x inside)
     fp = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -262,7 +280,7 @@ def main():
         e2e_val = float(ev[1]) / (float(em[0]) / 1e3)
 
     info = G.info
-    roof = roofline(G, prof_acc, info)
+    roof = roofline(G, sweep_ms, in_step)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
@@ -276,7 +294,7 @@ def main():
         "sizes": info,
         "setup_s": setup_s,
         "setup_phases_s": G.setup_times(),
-        "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof_acc.items()},
+        "phase_ms_one_solve_eager": {k: v[0] for k, v in prof.items()},
         "roofline": roof,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
@@ -294,26 +312,30 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(G, prof, info):
-    """Dominant kernel class of the step and its achieved HBM bandwidth against
-    the measured copy bandwidth (MEASURED_PEAKS.json)."""
-    peak, src = 6650.0, "fallback (B200_PROFILING.md)"
+def roofline(G, sweep_ms, in_step):
+    """Dominant kernel of the step -- the persistent supernodal sweep applying
+    M_AS (k_sweep, one launch per preconditioner application) -- against the
+    measured HBM copy bandwidth (MEASURED_PEAKS.json)."""
+    peak, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             peak = float(json.load(fh)["hbm_gbs"])
             src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         pass
-    # algorithmic bytes of one preconditioner application (DESIGN.md §5)
-    b = G.bytes_model()
-    name = "preconditioner M_AS,2 (local LDL^T sweeps + coarse + 2 SpMV)"
-    ms, cnt = prof.get("local_fwd", (0.0, 0))
-    if cnt == 0 or ms <= 0:
-        return None
-    achieved = b["precond"] / (ms / cnt / 1e3) / 1e9
-    return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_source": src,
-            "bytes_per_launch": b["precond"], "avg_launch_ms": ms / cnt}
+    b = G.bytes_model()["local"]
+    achieved = b / (sweep_ms / 1e3) / 1e9
+    traffic = None
+    try:  # DRAM bytes of one k_sweep (local) launch from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_sweep_local.json")) as fh:
+            traffic = float(json.load(fh)["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return {"bound": "hbm", "kernel": "k_sweep (local solves: gather, L y = b, D^-1, L^T x = z, prolong)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": src, "bytes_per_launch": b,
+            "avg_launch_ms": sweep_ms, "avg_launch_ms_in_step": in_step[0],
+            "launches_in_step": in_step[1]}
 
 
 if __name__ == "__main__":

@@ -189,6 +189,10 @@ enum {
   MDD_PROF_COUNT
 };
 int mdd_set_profiling(mdd_handle h, int enable);
+/* Device time accumulated inside the persistent sweep kernel (first CTA start to
+ * last CTA end, %globaltimer) over all its launches so far, and the launch count:
+ * which = 0 local solves (M_AS), 1 coarse solves (E^{-1}).  HOST outputs. */
+int mdd_sweep_timing(mdd_handle h, int which, double* ms_total, int64_t* launches);
 int mdd_profile(mdd_handle h, double* ms, int64_t* launches, int count);
 
 const char* mdd_last_error(void);

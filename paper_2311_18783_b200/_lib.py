@@ -43,7 +43,7 @@ EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_s
            "mdd_apply_preconditioner",
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_info",
            "mdd_get_int_array", "mdd_topology_int_array", "mdd_get_double_array",
-           "mdd_phase_name", "mdd_set_profiling", "mdd_profile", "mdd_last_error"]
+           "mdd_phase_name", "mdd_set_profiling", "mdd_sweep_timing", "mdd_profile", "mdd_last_error"]
 
 
 def load() -> C.CDLL:
@@ -71,6 +71,7 @@ def load() -> C.CDLL:
         "mdd_phase_name": (C.c_char_p, [C.c_int]),
         "mdd_set_profiling": (C.c_int, [P, C.c_int]),
         "mdd_profile": (C.c_int, [P, dp, lp, C.c_int]),
+        "mdd_sweep_timing": (C.c_int, [P, C.c_int, dp, lp]),
         "mdd_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():

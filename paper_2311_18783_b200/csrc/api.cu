@@ -1096,6 +1096,17 @@ int mdd_set_profiling(mdd_handle h, int enable) {
   });
 }
 
+int mdd_sweep_timing(mdd_handle h, int which, double* ms_total, int64_t* launches) {
+  if (!h || !ms_total || !launches) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    MDD_REQUIRE(which == 0 || (which == 1 && h->has_coarse), 2, "which must be 0 (local) or 1 (coarse)");
+    unsigned long long ns = 0, cnt = 0;
+    (which == 0 ? h->loc : h->crs).sweep_timing(&ns, &cnt, h->stream);
+    *ms_total = (double)ns * 1e-6;
+    *launches = (int64_t)cnt;
+  });
+}
+
 int mdd_profile(mdd_handle h, double* ms, int64_t* launches, int count) {
   if (!h) { g_err = "null argument"; return MDD_ERR_ARG; }
   for (int k = 0; k < count && k < MDD_PROF_COUNT; ++k) {

@@ -76,7 +76,8 @@ struct DevFactor {
   DBuf<int> ncol, noff, child_list, relmap, asm_pos, level_sn, parent;
   DBuf<double> L, dinv, upd, xf, xb;
   // persistent level-synchronous sweep (sweep.cu)
-  DBuf<int4> phases, mtask, tdesc, tiles;
+  DBuf<int4> phases, tdesc, tiles;
+  DBuf<dev::MTaskDesc> mt_f, mt_b;
   DBuf<int64_t> tile_off, sn_fpart, sn_bpart, vb_off, cptr, cidx, wsrc;
   DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc;
   DBuf<int32_t> gsrc;

@@ -139,12 +139,13 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     vcptr[q + 1] = (int64_t)vcidx.size();
   }
   std::vector<std::vector<int64_t>>().swap(contrib);
-  // ---- M tasks per level (largest first) and the phase list
-  std::vector<int4> mt, td, ph;
+  // ---- M tasks per level (largest first) with packed descriptors
+  std::vector<dev::MTaskDesc> mtf, mtb;
+  std::vector<int4> td;
   std::vector<int> mt_lev(fp.nlevels + 1, 0);
   for (int l = 0; l < fp.nlevels; ++l) {
-    mt_lev[l] = (int)mt.size();
-    std::vector<std::pair<int64_t, int4>> lt;  // (bytes, {g, tile, -, -})
+    mt_lev[l] = (int)mtf.size();
+    std::vector<std::pair<int64_t, int4>> lt;  // (bytes, {g, tile or -1})
     for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
       const int g = fp.level_sn[k];
       if (small[g]) {
@@ -158,16 +159,53 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     std::stable_sort(lt.begin(), lt.end(), [](const std::pair<int64_t, int4>& x,
                                               const std::pair<int64_t, int4>& y) { return x.first > y.first; });
     for (auto& e : lt) {
-      int4 m = e.second;
-      m.z = (int)td.size();
-      std::vector<int> ts = m.y < 0 ? sn_tiles[m.x] : std::vector<int>{m.y};
+      const int g = e.second.x, tt = e.second.y;
+      const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
+      dev::MTaskDesc D{};
+      D.col0 = fp.sn_col0[g];
+      D.vo = vvo[g];
+      D.uptr = fp.sn_uptr[g];
+      D.nr = nr; D.nc = nc; D.RB = vRB[g]; D.CB = vCB[g];
+      D.big = tt >= 0;
+      D.k0 = (int)td.size();
+      std::vector<int> ts = tt < 0 ? sn_tiles[g] : std::vector<int>{tt};
       for (int t : ts)
         td.push_back(make_int4(t, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
-      m.w = (int)td.size();
-      mt.push_back(m);
+      D.k1 = (int)td.size();
+      dev::MTaskDesc F = D, B = D;
+      auto set_vec = [](dev::MTaskDesc& X, int64_t lo, int64_t hi) {
+        X.vlo2 = lo & ~1LL;
+        X.voff = (int)(lo - X.vlo2);
+        X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
+      };
+      if (tt < 0) {
+        F.rows = B.rows = nr;
+        F.cols = B.cols = nc;
+        set_vec(F, vvo[g], vvo[g] + nr);
+        set_vec(B, vvo[g], vvo[g] + nr);
+      } else {
+        const int rb = tl[tt].y, cb = tl[tt].z, RB = vRB[g], CB = vCB[g];
+        const int rows = std::min(RB, nr - rb * RB), cols = std::min(CB, nc - cb * CB);
+        const int rend = std::min(nr, (rb + 1) * RB);
+        const int rb0 = (cb * CB) / RB;
+        F.rb = B.rb = rb; F.cb = B.cb = cb; F.rows = B.rows = rows; F.cols = B.cols = cols;
+        F.part = vfp[g] + (int64_t)cb * nr + (int64_t)rb * RB;
+        F.comb = vfp[g] + (int64_t)rb * RB;
+        F.cnt = vrbc[g] + rb;
+        F.ntl = std::min(vncb[g], (rend + CB - 1) / CB);
+        set_vec(F, vvo[g] + (int64_t)cb * CB, vvo[g] + (int64_t)cb * CB + cols);
+        B.part = vbp[g] + (int64_t)rb * nc + (int64_t)cb * CB;
+        B.comb = vbp[g] + (int64_t)rb0 * nc + (int64_t)cb * CB;
+        B.cnt = vcbc[g] + cb;
+        B.ntl = vnrb[g] - rb0;
+        set_vec(B, vvo[g] + (int64_t)rb * RB, vvo[g] + (int64_t)rb * RB + rows);
+      }
+      mtf.push_back(F);
+      mtb.push_back(B);
     }
   }
-  mt_lev[fp.nlevels] = (int)mt.size();
+  mt_lev[fp.nlevels] = (int)mtf.size();
+  std::vector<int4> ph;
   int nm = 0;
   for (int l = 0; l < fp.nlevels; ++l) {
     ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
@@ -187,7 +225,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   nphases = (int)ph.size();
   MDD_REQUIRE(nrows < INT32_MAX, 5, "sweep row space too large for 32-bit phase bounds");
   phases.upload(ph);
-  mtask.upload(mt);
+  mt_f.upload(mtf);
+  mt_b.upload(mtb);
   tdesc.upload(td);
   tiles.upload(tl);
   tile_off.upload(toff);
@@ -199,7 +238,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   cptr.upload(vcptr);
   cidx.upload(vcidx.empty() ? std::vector<int64_t>{0} : vcidx);
   wsrc.upload(vwsrc);
-  vb.alloc(std::max<int64_t>(nrows, 1));
+  vb.alloc(nrows + 2);  // +2: the even-aligned bulk copies may read one past the end
   fpart.alloc(std::max<int64_t>(nfp, 1));
   bpart.alloc(std::max<int64_t>(nbp, 1));
   rb_cnt.alloc(std::max(nrbc, 1));
@@ -225,7 +264,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     for (int g = 0; g < nsn; ++g) nbig += !small[g];
     fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) mtasks %d "
             "rows %lld contrib %lld grid %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(),
-            ntiles, 100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), (int)mt.size(),
+            ntiles, 100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), (int)mtf.size(),
             (long long)nrows, (long long)vcidx.size(), sweep_grid);
     for (int l = 0; l < fp.nlevels; ++l) {
       long long ent = 0;
@@ -258,7 +297,8 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.phases = phases.p;
   S.nphases = nphases;
   S.ticket = ticket.p;
-  S.mtask = mtask.p;
+  S.mtf = mt_f.p;
+  S.mtb = mt_b.p;
   S.tdesc = tdesc.p;
   S.tiles = tiles.p;
   S.tile_off = tile_off.p;

@@ -260,6 +260,14 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
     for (int q = j; q < nc; ++q) s += F[(i64)q * nr + i] * Lp[(i64)j * nr + q];
     Lp[(i64)j * nr + i] = s;
   }
+  __syncthreads();
+  // fold D^{-1} into the rows of the diagonal block: the forward sweep then yields
+  // z_c = D^{-1} L11^{-1} t_c directly; the backward sweep divides z_c by D^{-1}
+  // again in its gather (sweep.cu, G_b)
+  for (i64 k = tid; k < (i64)nc * nc; k += nt) {
+    const int j = (int)(k / nc), i = (int)(k % nc);
+    if (i >= j) Lp[(i64)j * nr + i] *= dinv[col0 + i];
+  }
 }
 
 __global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,

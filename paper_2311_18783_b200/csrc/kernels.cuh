@@ -93,19 +93,36 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
 enum { SW_EPOCH = 0, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR };
 constexpr int kSweepThreads = 256;
-constexpr int kTileMax = 4096;   // doubles per tile (32 KB, one TMA bulk copy)
+constexpr int kTileMax = 3840;   // doubles per tile (30 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
-constexpr int kSweepSmemDoubles = 2 * kTileMax + 2 * kVecMax + kSweepThreads;
+constexpr int kSweepSmemDoubles = 2 * kTileMax + 3 * kVecMax + 4 + kSweepThreads;
+
+// one task of an M phase (factor_driver.cu builds them, forward and backward)
+struct __align__(16) MTaskDesc {
+  long long col0;   // position of the supernode's first column
+  long long vo;     // vb offset of the supernode's rows
+  long long vlo2;   // even-aligned start of the task vector's bulk copy (vb index)
+  long long uptr;   // offset of the supernode's update vector
+  long long part;   // big: offset of this tile's partial sums (fpart / bpart)
+  long long comb;   // big: first partial of the combine (row block / column block)
+  long long cnt;    // big: index of the row-block / column-block counter
+  int big, k0, k1;  // small / big tile; tdesc range
+  int nr, nc, rows, cols, rb, cb, RB, CB;
+  int ntl;          // big: tiles combined by the last arriver
+  int voff;         // offset of the vector inside its shared-memory buffer
+  int vbytes;       // bytes of the vector bulk copy
+};
 
 struct SweepDev {
   PlanDev P;
   const double* dinv;
+  const MTaskDesc* mtf;          // M tasks, forward / backward descriptors
+  const MTaskDesc* mtb;
   // phases {kind, a, b, ticket slot}: G: rows [a, b) of vb; M: mtask [a, b); PR
   const int4* phases;
   int nphases;
-  unsigned long long* ticket;    // one cumulative ticket counter per M phase
-  const int4* mtask;             // {supernode, tile (-1: small supernode), tdesc [first, end)}
+  unsigned long long* ticket;    // (unused: M tasks are dealt statically)
   const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
   const int64_t* tile_off;       // into Lt

@@ -8,10 +8,10 @@
 // sum_i R_i^T x_i (PAPER.md eq. AS: M_AS = sum_i R_i^T A_i^{-1} R_i).  The same
 // kernel applies E^{-1} for the coarse correction Z E^{-1} Z^T.
 //
-// Panels are in "partitioned-inverse" form P = [L11^{-1}; L21 L11^{-1}], so per
-// supernode
-//   forward :  z_c = D^{-1} (L11^{-1} t_c),     u = t_off - (L21 L11^{-1}) t_c
-//   backward:  x_c = L11^{-T} z_c - (L21 L11^{-1})^T x_off
+// Panels are in "partitioned-inverse" form P = [D^{-1} L11^{-1}; L21 L11^{-1}], so
+// per supernode
+//   forward :  z_c = (D^{-1} L11^{-1}) t_c,     u = t_off - (L21 L11^{-1}) t_c
+//   backward:  x_c = (D^{-1} L11^{-1})^T (D z_c) - (L21 L11^{-1})^T x_off
 // are plain dense mat-vecs over contiguous tiles (<= kTileMax doubles), each
 // streamed from HBM by ONE TMA bulk copy (cp.async.bulk + mbarrier) with one
 // task of look-ahead.
@@ -21,7 +21,7 @@
 //   for each level, leaves first:   G_f  (flat gather of every supernode's
 //     right-hand side t = [b_c ; 0] + children's update vectors, a precomputed
 //     row -> contributions list, so no scatter and no atomics)  |  M_f (tiles)
-//   for each level, root first:     G_b  (w = [z_c ; -x_off])  |  M_b (tiles)
+//   for each level, root first:     G_b  (w = [D z_c ; -x_off])  |  M_b (tiles)
 //   prolongation.
 // Within M phases CTAs take tasks from an atomic ticket (largest first).  A task
 // is either a small supernode (all its column tiles, accumulated in shared
@@ -179,9 +179,10 @@ __device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, con
 
 __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   extern __shared__ __align__(128) double sm[];
-  double* const vec = sm + 2 * kTileMax;   // kVecMax
-  double* const vec2 = vec + kVecMax;      // kVecMax
-  double* const red = vec2 + kVecMax;      // kSweepThreads
+  double* const vbuf0 = sm + 2 * kTileMax;  // kVecMax + 2: task vectors (double-buffered)
+  double* const vbuf1 = vbuf0 + kVecMax + 2;
+  double* const vec2 = vbuf1 + kVecMax + 2;   // kVecMax: accumulators
+  double* const red = vec2 + kVecMax;         // kSweepThreads
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ int s_next[2];
   __shared__ int s_flag;
@@ -215,10 +216,10 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         S.vb[q] = v;
       }
     } else if (kind == PH_GB) {
-      // w = [z_c ; -x_off]
+      // w = [D z_c ; -x_off]
       for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) {
         const i64 w = S.wsrc[q];
-        S.vb[q] = w >= 0 ? __ldcg(S.xf + w) : -__ldcg(S.xb + (-w - 1));
+        S.vb[q] = w >= 0 ? __ldcg(S.xf + w) / __ldg(S.dinv + w) : -__ldcg(S.xb + (-w - 1));
       }
     } else if (kind == PH_PR) {
       for (size_t e = gtid; e < (size_t)S.n_out; e += gthreads) {
@@ -227,122 +228,120 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         S.out[e] = s;
       }
     } else if (!*(volatile unsigned long long*)&S.ctl[SW_ABORT]) {
-      // ---------------------------------------------- M phase: tiles
+      // ---------------------------------------------- M phase: tiles.  Tasks are
+      // sorted largest first and dealt to the CTAs in snake order (no atomics);
+      // every per-task quantity comes from one packed descriptor.
       const bool fwd = kind == PH_MF;
-      const int ta = PH.y, ntk = PH.z - PH.y;
-      const unsigned long long base = (cur - 1) * ((unsigned long long)ntk + grid);
-      unsigned long long* tick = &S.ticket[PH.w];
-      auto prefetch_k = [&](int k, int b) {
-        const int4 d = S.tdesc[k];
-        const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
-        bulk_load(sm + b * kTileMax, S.Lt + off, (uint32_t)d.y, &mbar[b]);
+      const MTaskDesc* const MT = (fwd ? S.mtf : S.mtb) + PH.y;
+      const int ntk = PH.z - PH.y;
+      const int b = blockIdx.x, G = gridDim.x;
+      auto task_of = [&](int i) -> int {
+        const int k = (i & 1) ? i * G + (G - 1 - b) : i * G + b;
+        return k < ntk ? k : -1;
       };
-      int tn = 0;
+      // thread 0: stream tdesc[kk] into stage `bf`, plus (vbytes > 0) a task vector
+      auto prefetch = [&](int kk, int bf, long long vlo2, int vbytes, int vs) {
+        const int4 d = S.tdesc[kk];
+        const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[bf])),
+                     "r"((uint32_t)d.y + (uint32_t)vbytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sm + bf * kTileMax)),
+            "l"(S.Lt + off), "r"((uint32_t)d.y), "r"(smem_u32(&mbar[bf]))
+            : "memory");
+        if (vbytes > 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(vs ? vbuf1 : vbuf0)),
+              "l"(S.vb + vlo2), "r"((uint32_t)vbytes), "r"(smem_u32(&mbar[bf]))
+              : "memory");
+      };
       if (tid == 0) {
-        const int k0 = (int)(atomicAdd(tick, 1ull) - base);
-        s_next[0] = k0;
-        if (k0 < ntk) prefetch_k(S.mtask[ta + k0].z, buf);
+        const int k0 = task_of(0);
+        if (k0 >= 0) prefetch(MT[k0].k0, buf, MT[k0].vlo2, MT[k0].vbytes, 0);
       }
-      __syncthreads();
-      for (int it = 0;; ++it) {
-        const int k = s_next[it & 1];
-        if (k >= ntk) break;
-        const int4 mt = S.mtask[ta + k];  // {supernode, tile (-1: small), first tdesc, end tdesc}
+      for (int i = 0;; ++i) {
+        const int k = task_of(i);
+        if (k < 0) break;
+        const MTaskDesc D = MT[k];
+        const int vs = i & 1;
+        // thread 0: what to stream after this task's last tile
+        int nk0 = -1, nvb = 0;
+        long long nvlo = 0;
         if (tid == 0) {
-          tn = (int)(atomicAdd(tick, 1ull) - base);
-          s_next[(it + 1) & 1] = tn;
+          const int kn = task_of(i + 1);
+          if (kn >= 0) { nk0 = MT[kn].k0; nvlo = MT[kn].vlo2; nvb = MT[kn].vbytes; }
         }
-        const int g = mt.x;
-        const i64 col0 = P.sn_col0[g];
-        const i64 vo = S.vb_off[g];
-        // wait for the tile in `buf`; stream the next one (this task's or the next
-        // task's first) into buf ^ 1
+        const double* const vv = (vs ? vbuf1 : vbuf0) + D.voff;  // this task's vector
         auto next_tile_and_wait = [&](int kk) {
           if (tid == 0) {
-            const int nk = kk + 1 < mt.w ? kk + 1 : (tn < ntk ? S.mtask[ta + tn].z : -1);
-            if (nk >= 0) prefetch_k(nk, buf ^ 1);
+            if (kk + 1 < D.k1) prefetch(kk + 1, buf ^ 1, 0, 0, 0);
+            else if (nk0 >= 0) prefetch(nk0, buf ^ 1, nvlo, nvb, vs ^ 1);
           }
           if (buf) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
           else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
         };
-        if (mt.y < 0) {
+        if (!D.big) {
           // ---------------- small supernode: all column tiles, one CTA
-          const TileGeo G0 = geo(S, g, 0, 0);
-          for (int q = tid; q < G0.nr; q += kSweepThreads) {
-            vec[q] = __ldcg(S.vb + vo + q);
-            vec2[q] = 0.0;
-          }
-          __syncthreads();
-          for (int kk = mt.z; kk < mt.w; ++kk) {
-            const int cb = S.tiles[S.tdesc[kk].x].z;
-            const TileGeo G = geo(S, g, 0, cb);
+          for (int kk = D.k0; kk < D.k1; ++kk) {
+            const int cb = kk - D.k0;
+            const int cols = min(D.CB, D.nc - cb * D.CB);
             next_tile_and_wait(kk);
             const double* T = sm + buf * kTileMax;
             if (fwd) {
-              tile_matvec(T, G.rows, G.cols, vec + cb * G.CB, red, [&](int i, double y) { vec2[i] += y; });
+              if (cb == 0)
+                tile_matvec(T, D.nr, cols, vv, red, [&](int r, double y) { vec2[r] = y; });
+              else
+                tile_matvec(T, D.nr, cols, vv + cb * D.CB, red, [&](int r, double y) { vec2[r] += y; });
             } else {
-              double* const xb = S.xb + col0 + cb * G.CB;
-              tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { xb[j] = y; });
+              double* const xb = S.xb + D.col0 + cb * D.CB;
+              tile_matvec_t(T, D.nr, cols, vv, [&](int j, double y) { xb[j] = y; });
             }
             __syncthreads();
             buf ^= 1;
           }
           if (fwd) {
-            double* const upd = S.upd + P.sn_uptr[g];
-            for (int i = tid; i < G0.nr; i += kSweepThreads) {
-              if (i < G0.nc) S.xf[col0 + i] = __ldg(S.dinv + col0 + i) * vec2[i];
-              else upd[i - G0.nc] = vec[i] - vec2[i];
+            double* const upd = S.upd + D.uptr;
+            for (int r = tid; r < D.nr; r += kSweepThreads) {
+              if (r < D.nc) S.xf[D.col0 + r] = vec2[r];
+              else upd[r - D.nc] = vv[r] - vec2[r];
             }
           }
         } else {
           // ---------------- one tile of a big supernode
-          const int4 tl = S.tiles[mt.y];
-          const int rb = tl.y, cb = tl.z;
-          const TileGeo G = geo(S, g, rb, cb);
-          if (fwd) {
-            for (int q = tid; q < G.cols; q += kSweepThreads) vec[q] = __ldcg(S.vb + vo + cb * G.CB + q);
-          } else {
-            for (int q = tid; q < G.rows; q += kSweepThreads) vec[q] = __ldcg(S.vb + vo + rb * G.RB + q);
-          }
-          __syncthreads();
-          next_tile_and_wait(mt.z);
+          next_tile_and_wait(D.k0);
           const double* T = sm + buf * kTileMax;
-          if (fwd) {
-            double* fp = S.fpart + S.sn_fpart[g] + (i64)cb * G.nr + (i64)rb * G.RB;
-            tile_matvec(T, G.rows, G.cols, vec, red, [&](int i, double y) { fp[i] = y; });
-          } else {
-            double* bp = S.bpart + S.sn_bpart[g] + (i64)rb * G.nc + (i64)cb * G.CB;
-            tile_matvec_t(T, G.rows, G.cols, vec, [&](int j, double y) { bp[j] = y; });
-          }
+          double* const part = (fwd ? S.fpart : S.bpart) + D.part;
+          if (fwd) tile_matvec(T, D.rows, D.cols, vv, red, [&](int r, double y) { part[r] = y; });
+          else tile_matvec_t(T, D.rows, D.cols, vv, [&](int j, double y) { part[j] = y; });
           __syncthreads();
           buf ^= 1;
-          const int rend = min(G.nr, (rb + 1) * G.RB);
-          const int ntl = fwd ? min(G.ncb, (rend + G.CB - 1) / G.CB) : G.nrb - (cb * G.CB) / G.RB;
           if (tid == 0) {
             __threadfence();
-            unsigned long long* c = fwd ? &S.rb_cnt[S.sn_rbc[g] + rb] : &S.cb_cnt[S.sn_cbc[g] + cb];
-            s_flag = atomicAdd(c, 1ull) + 1 == cur * (unsigned long long)ntl;
+            unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
+            s_flag = atomicAdd(c, 1ull) + 1 == cur * (unsigned long long)D.ntl;
             __threadfence();
           }
           __syncthreads();
           if (s_flag) {
             // last tile of its row block (fwd) / column block (bwd): fixed-order combine
             if (fwd) {
-              const double* fb = S.fpart + S.sn_fpart[g] + (i64)rb * G.RB;
-              for (int i = tid; i < G.rows; i += kSweepThreads) {
-                double s = 0.0;
-                for (int q = 0; q < ntl; ++q) s += __ldcg(fb + (i64)q * G.nr + i);
-                const int r = rb * G.RB + i;
-                if (r < G.nc) S.xf[col0 + r] = __ldg(S.dinv + col0 + r) * s;
-                else S.upd[P.sn_uptr[g] + (r - G.nc)] = __ldcg(S.vb + vo + r) - s;
+              const double* fb = S.fpart + D.comb;
+              for (int i2 = tid; i2 < D.rows; i2 += kSweepThreads) {
+                double sum = 0.0;
+                for (int q = 0; q < D.ntl; ++q) sum += __ldcg(fb + (i64)q * D.nr + i2);
+                const int r = D.rb * D.RB + i2;
+                if (r < D.nc) S.xf[D.col0 + r] = sum;
+                else S.upd[D.uptr + (r - D.nc)] = __ldcg(S.vb + D.vo + r) - sum;
               }
             } else {
-              const int rb0 = (cb * G.CB) / G.RB;
-              const double* bb = S.bpart + S.sn_bpart[g] + (i64)cb * G.CB;
-              for (int j = tid; j < G.cols; j += kSweepThreads) {
-                double s = 0.0;
-                for (int q = rb0; q < G.nrb; ++q) s += __ldcg(bb + (i64)q * G.nc + j);
-                S.xb[col0 + cb * G.CB + j] = s;
+              const double* bb = S.bpart + D.comb;
+              for (int j = tid; j < D.cols; j += kSweepThreads) {
+                double sum = 0.0;
+                for (int q = 0; q < D.ntl; ++q) sum += __ldcg(bb + (i64)q * D.nc + j);
+                S.xb[D.col0 + D.cb * D.CB + j] = sum;
               }
             }
           }

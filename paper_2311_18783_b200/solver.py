@@ -148,7 +148,9 @@ class MaxwellDD:
         i = self.info
         n, nnzA, nloc = i["n"], i["nnz_A"], i["nloc"]
         spmv = 12 * nnzA + 8 * (n + 1) + 16 * n
-        local = 2 * 8 * i["local_factor_nnz"] + 8 * nloc + 4 * nloc + 3 * 8 * nloc + 8 * n + 8 * n
+        # local sweep: every factor entry once per direction, D^{-1}, the restriction
+        # of r and the prolongated result (the kernel's own scratch is not counted)
+        local = 2 * 8 * i["local_factor_nnz"] + 8 * nloc + 8 * n + 8 * n
         coarse = (2 * 12 * i["nnz_Z"] + 2 * 8 * i["coarse_factor_nnz"] + 8 * i["n0"] + 16 * n) \
             if i["n0"] else 0
         vec = 8 * n * 4
@@ -170,6 +172,13 @@ class MaxwellDD:
 
     def set_profiling(self, on=True):
         L.check(L.lib().mdd_set_profiling(self._h, 1 if on else 0))
+
+    def sweep_timing(self, which="local"):
+        """(total device ms, launches) of the persistent sweep kernel so far."""
+        ms = C.c_double(0.0)
+        n = C.c_int64(0)
+        L.check(L.lib().mdd_sweep_timing(self._h, 0 if which == "local" else 1, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def profile(self):
         ms = (C.c_double * len(L.PROF_NAMES))()
