@@ -233,11 +233,11 @@ struct mdd_solver {
   }
 
   // ------------------------------------------------------------ helpers
+  // A x with 8 lanes per row on an SM-sized grid (nparts blocks: the fused dot's
+  // partials are reduced by one small kernel)
   void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
             double* out, const double* dotw = nullptr, double* part_ = nullptr) {
-    int warps_per_block = 8;
-    dev::k_spmv<<<nblk(rows, warps_per_block), 32 * warps_per_block, 0, stream>>>(
-        rows, ptr, idx, val, in, out, dotw, part_, state.p);
+    dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, out, dotw, part_, state.p);
     launches += 1;
   }
   void applyA(const double* in, double* out) {
@@ -250,11 +250,11 @@ struct mdd_solver {
     launches += 1;
   }
   void apply_coarse(const double* v, double* y) {
-    dev::k_csr_warp_spmv<<<nblk(n0 * 32, 256), 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p,
-                                                                 Zt_val.p, v, xc.p, state.p);
+    dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p, Zt_val.p, v, xc.p,
+                                                   nullptr, nullptr, state.p);
     crs.sweep(xc.p, nullptr, stream, state.p);
-    dev::k_csr_warp_spmv<<<nblk((int64_t)n * 32, 256), 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p,
-                                                                         crs.xb.p, y, state.p);
+    dev::k_spmv16<<<nparts, 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p, crs.xb.p, y, nullptr,
+                                                   nullptr, state.p);
     launches += 3;
   }
   void apply_prec(const double* rr, double* zz) {
@@ -306,12 +306,10 @@ struct mdd_solver {
   // one PCG iteration; every kernel is a no-op once state[ST_STOP] is set.
   // marks: optional event indices for the eager profiling path
   void enqueue_body(const std::function<void(int)>& mark) {
-    const int blocks = nblk(n, 8);
     if (mark) mark(2);
-    dev::k_spmv<<<blocks, 256, 0, stream>>>(n, A_ptr.p, A_idx.p, A_val.p, p.p, q.p, p.p, part.p, state.p);
-    launches += 1;
+    spmv(A_ptr.p, A_idx.p, A_val.p, n, p.p, q.p, p.p, part.p);
     if (mark) mark(3);
-    dev::k_reduce<<<1, 256, 0, stream>>>(blocks, part.p, S.p + dev::S_PQ, state.p);
+    dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + dev::S_PQ, state.p);
     launches += 1;
     scalar(0);
     dev::k_update_xr<<<nparts, 256, 0, stream>>>(n, x.p, r.p, p.p, q.p, S.p, part.p, state.p);
@@ -807,7 +805,12 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
   H->xloc.alloc(H->loc.fp.ntot);
   H->xc.alloc(std::max<int64_t>(H->n0, 1));
   H->S.alloc(dev::S_COUNT);
-  H->nparts = 4 * 148;
+  {
+    int dev_id = 0, nsm = 0;
+    CUDA_CHECK(cudaGetDevice(&dev_id));
+    CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
+    H->nparts = 8 * nsm;  // SM-sized grid of the streaming kernels and their partial sums
+  }
   H->part.alloc(std::max<int64_t>(H->nparts, nblk(n, 8)) + 8);
   H->state.alloc(dev::ST_COUNT);
   H->state.zero(s);

@@ -53,55 +53,64 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   upd.alloc(std::max<int64_t>(fp.usize, 1));
   xf.alloc(std::max<int64_t>(fp.ntot, 1));
   xb.alloc(std::max<int64_t>(fp.ntot, 1));
-  // ---- tile geometry.  "small": one CTA sweeps the whole panel (column tiles over
-  // all nr rows, accumulated in shared memory); "big": RB x CB tiles spread over
-  // CTAs, partial sums combined by the last tile of a row / column block
+  // ---- tile geometry.  small: one CTA sweeps the whole panel (column tiles over
+  // all nr rows, accumulated in shared memory).  strip (big, nr <= kVecMax):
+  // forward row strips x all columns and backward all rows x column strips (two
+  // copies of the panel; no partial sums).  2-D (nr > kVecMax): RB x CB tiles
+  // whose partial sums the last tile of a row / column block combines.
+  // tiles[] = {g, a, b, kind}: kind 0 = 2-D (a = rb, b = cb), 1 = forward strip
+  // (a = first row), 2 = backward strip (b = first column), 3 = small column tile
   const int nsn = fp.nsn;
-  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn), vncb(nsn), vrbc(nsn, 0), vcbc(nsn, 0);
-  std::vector<uint8_t> small(nsn);
+  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn, 1), vncb(nsn, 1), vrbc(nsn, 0), vcbc(nsn, 0);
+  std::vector<uint8_t> mode(nsn);  // 0 small, 1 strip, 2 2-D
   std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0);
-  std::vector<std::vector<int>> sn_tiles(nsn);
+  std::vector<std::vector<int>> ft(nsn), bt(nsn);  // forward / backward tiles (2-D: same list)
   std::vector<int4> tl;
+  std::vector<int2> rc;  // rows x cols of each tile
   std::vector<int64_t> toff;
   int64_t off = 0, nfp = 0, nbp = 0;
   int nrbc = 0, ncbc = 0;
+  auto add_tile = [&](int4 t, int rows, int cols) {
+    tl.push_back(t);
+    rc.push_back(make_int2(rows, cols));
+    toff.push_back(off);
+    off += ((int64_t)rows * cols + 1) & ~1LL;  // 16-byte aligned tiles
+    return (int)tl.size() - 1;
+  };
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
-    small[g] = nr <= dev::kVecMax && (int64_t)nr * nc <= dev::kSingleMax;
-    int RB, CB;
-    if (small[g]) {
-      RB = nr;
-      CB = std::max(1, std::min(nc, dev::kTileMax / nr));
+    mode[g] = nr <= dev::kVecMax ? ((int64_t)nr * nc <= dev::kSingleMax ? 0 : 1) : 2;
+    if (mode[g] == 0) {
+      const int CB = std::max(1, std::min(nc, dev::kTileMax / nr));
+      vRB[g] = nr; vCB[g] = CB;
+      for (int c0 = 0; c0 < nc; c0 += CB) ft[g].push_back(add_tile(make_int4(g, 0, c0, 3), nr, std::min(CB, nc - c0)));
+      bt[g] = ft[g];
+    } else if (mode[g] == 1) {
+      const int rs = std::max(1, dev::kTileMax / nc), cs = std::max(1, dev::kTileMax / nr);
+      vRB[g] = rs; vCB[g] = cs;
+      for (int r0 = 0; r0 < nr; r0 += rs) ft[g].push_back(add_tile(make_int4(g, r0, 0, 1), std::min(rs, nr - r0), nc));
+      for (int c0 = 0; c0 < nc; c0 += cs) bt[g].push_back(add_tile(make_int4(g, 0, c0, 2), nr, std::min(cs, nc - c0)));
     } else {
-      CB = std::min(nc, 64);
-      RB = std::min(dev::kVecMax, std::max(32, (dev::kTileMax / CB) / 32 * 32));
-    }
-    const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
-    vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
-    if (!small[g]) {
+      const int CB = std::min(nc, 64);
+      const int RB = std::min(dev::kVecMax, std::max(32, (dev::kTileMax / CB) / 32 * 32));
+      const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
+      vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;
       vbp[g] = nbp; nbp += (int64_t)nrb * nc;
       vrbc[g] = nrbc; nrbc += nrb;
       vcbc[g] = ncbc; ncbc += ncb;
-    }
-    for (int rb = 0; rb < nrb; ++rb) {
-      const int rend = std::min(nr, (rb + 1) * RB), rows = rend - rb * RB;
-      for (int cb = 0; cb < ncb && cb * CB < rend; ++cb) {
-        const int cols = std::min(CB, nc - cb * CB);
-        sn_tiles[g].push_back((int)tl.size());
-        tl.push_back(make_int4(g, rb, cb, 0));
-        toff.push_back(off);
-        off += ((int64_t)rows * cols + 1) & ~1LL;  // 16-byte aligned tiles
+      for (int rb = 0; rb < nrb; ++rb) {
+        const int rend = std::min(nr, (rb + 1) * RB), rows = rend - rb * RB;
+        for (int cb = 0; cb < ncb && cb * CB < rend; ++cb)
+          ft[g].push_back(add_tile(make_int4(g, rb, cb, 0), rows, std::min(CB, nc - cb * CB)));
       }
+      bt[g] = ft[g];
     }
   }
   ntiles = (int)tl.size();
   lt_size = off;
   auto tile_bytes = [&](int t) {
-    const int4 q = tl[t];
-    const int g = q.x, nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
-    const int rows = std::min(vRB[g], nr - q.y * vRB[g]), cols = std::min(vCB[g], nc - q.z * vCB[g]);
-    return (int)((((int64_t)rows * cols + 1) & ~1LL) * (int64_t)sizeof(double));
+    return (int)((((int64_t)rc[t].x * rc[t].y + 1) & ~1LL) * (int64_t)sizeof(double));
   };
   // ---- per-level row vectors: rows of g at vb_off[g], each level contiguous
   std::vector<int64_t> vvo(nsn), lev_row(fp.nlevels + 1, 0);
@@ -139,81 +148,112 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     vcptr[q + 1] = (int64_t)vcidx.size();
   }
   std::vector<std::vector<int64_t>>().swap(contrib);
-  // ---- M tasks per level (largest first) with packed descriptors
+  // ---- M tasks per level and direction (largest first), packed descriptors
   std::vector<dev::MTaskDesc> mtf, mtb;
   std::vector<int4> td;
-  std::vector<int> mt_lev(fp.nlevels + 1, 0);
-  for (int l = 0; l < fp.nlevels; ++l) {
-    mt_lev[l] = (int)mtf.size();
-    std::vector<std::pair<int64_t, int4>> lt;  // (bytes, {g, tile or -1})
-    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-      const int g = fp.level_sn[k];
-      if (small[g]) {
-        int64_t by = 0;
-        for (int t : sn_tiles[g]) by += tile_bytes(t);
-        lt.push_back({by, make_int4(g, -1, 0, 0)});
-      } else {
-        for (int t : sn_tiles[g]) lt.push_back({tile_bytes(t), make_int4(g, t, 0, 0)});
+  std::vector<int> lev_f(fp.nlevels + 1, 0), lev_b(fp.nlevels + 1, 0);
+  auto push_td = [&](int t) {
+    td.push_back(make_int4(t, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
+  };
+  auto set_vec = [](dev::MTaskDesc& X, int64_t lo, int64_t hi) {
+    X.vlo2 = lo & ~1LL;
+    X.voff = (int)(lo - X.vlo2);
+    X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
+  };
+  for (int dir = 0; dir < 2; ++dir) {
+    std::vector<dev::MTaskDesc>& out = dir == 0 ? mtf : mtb;
+    std::vector<int>& lev = dir == 0 ? lev_f : lev_b;
+    for (int l = 0; l < fp.nlevels; ++l) {
+      lev[l] = (int)out.size();
+      std::vector<std::pair<int64_t, dev::MTaskDesc>> lt;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
+        dev::MTaskDesc D{};
+        D.col0 = fp.sn_col0[g];
+        D.vo = vvo[g];
+        D.uptr = fp.sn_uptr[g];
+        D.nr = nr; D.nc = nc; D.RB = vRB[g]; D.CB = vCB[g];
+        const std::vector<int>& tiles_g = dir == 0 ? ft[g] : bt[g];
+        if (mode[g] == 0) {
+          D.big = 0;
+          D.rows = nr; D.cols = nc;
+          set_vec(D, vvo[g], vvo[g] + nr);
+          int64_t by = 0;
+          for (int t : tiles_g) by += tile_bytes(t);
+          D.k0 = -1;
+          D.k1 = (int)tiles_g.size();  // resolved to tdesc ranges below
+          D.part = tiles_g.empty() ? -1 : tiles_g[0];
+          lt.push_back({by, D});
+        } else {
+          for (int t : tiles_g) {
+            dev::MTaskDesc X = D;
+            X.big = mode[g] == 1 ? 2 : 1;
+            X.rows = rc[t].x; X.cols = rc[t].y;
+            X.k0 = -2;
+            X.part = t;  // tile, resolved below
+            if (mode[g] == 1) {
+              X.rb = tl[t].y;
+              X.cb = tl[t].z;
+              set_vec(X, vvo[g], vvo[g] + nr);
+            } else {
+              const int rb = tl[t].y, cb = tl[t].z, RB = vRB[g], CB = vCB[g];
+              const int rend = std::min(nr, (rb + 1) * RB);
+              const int rb0 = (cb * CB) / RB;
+              X.rb = rb; X.cb = cb;
+              if (dir == 0) {
+                X.comb = vfp[g] + (int64_t)rb * RB;
+                X.cnt = vrbc[g] + rb;
+                X.ntl = std::min(vncb[g], (rend + CB - 1) / CB);
+                set_vec(X, vvo[g] + (int64_t)cb * CB, vvo[g] + (int64_t)cb * CB + X.cols);
+              } else {
+                X.comb = vbp[g] + (int64_t)rb0 * nc + (int64_t)cb * CB;
+                X.cnt = vcbc[g] + cb;
+                X.ntl = vnrb[g] - rb0;
+                set_vec(X, vvo[g] + (int64_t)rb * RB, vvo[g] + (int64_t)rb * RB + X.rows);
+              }
+            }
+            lt.push_back({tile_bytes(t), X});
+          }
+        }
+      }
+      std::stable_sort(lt.begin(), lt.end(), [](const std::pair<int64_t, dev::MTaskDesc>& x,
+                                                const std::pair<int64_t, dev::MTaskDesc>& y) { return x.first > y.first; });
+      for (auto& e : lt) {
+        dev::MTaskDesc X = e.second;
+        const int g = tl[(int)X.part].x;
+        if (X.k0 == -1) {  // small: all its column tiles
+          X.k0 = (int)td.size();
+          for (int t : (dir == 0 ? ft[g] : bt[g])) push_td(t);
+          X.k1 = (int)td.size();
+          X.part = 0;
+        } else {
+          const int t = (int)X.part;
+          X.k0 = (int)td.size();
+          push_td(t);
+          X.k1 = (int)td.size();
+          if (X.big == 1) {
+            const int nr = X.nr, nc = X.nc;
+            X.part = dir == 0 ? vfp[g] + (int64_t)X.cb * nr + (int64_t)X.rb * X.RB
+                              : vbp[g] + (int64_t)X.rb * nc + (int64_t)X.cb * X.CB;
+          } else {
+            X.part = 0;
+          }
+        }
+        out.push_back(X);
       }
     }
-    std::stable_sort(lt.begin(), lt.end(), [](const std::pair<int64_t, int4>& x,
-                                              const std::pair<int64_t, int4>& y) { return x.first > y.first; });
-    for (auto& e : lt) {
-      const int g = e.second.x, tt = e.second.y;
-      const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
-      dev::MTaskDesc D{};
-      D.col0 = fp.sn_col0[g];
-      D.vo = vvo[g];
-      D.uptr = fp.sn_uptr[g];
-      D.nr = nr; D.nc = nc; D.RB = vRB[g]; D.CB = vCB[g];
-      D.big = tt >= 0;
-      D.k0 = (int)td.size();
-      std::vector<int> ts = tt < 0 ? sn_tiles[g] : std::vector<int>{tt};
-      for (int t : ts)
-        td.push_back(make_int4(t, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
-      D.k1 = (int)td.size();
-      dev::MTaskDesc F = D, B = D;
-      auto set_vec = [](dev::MTaskDesc& X, int64_t lo, int64_t hi) {
-        X.vlo2 = lo & ~1LL;
-        X.voff = (int)(lo - X.vlo2);
-        X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
-      };
-      if (tt < 0) {
-        F.rows = B.rows = nr;
-        F.cols = B.cols = nc;
-        set_vec(F, vvo[g], vvo[g] + nr);
-        set_vec(B, vvo[g], vvo[g] + nr);
-      } else {
-        const int rb = tl[tt].y, cb = tl[tt].z, RB = vRB[g], CB = vCB[g];
-        const int rows = std::min(RB, nr - rb * RB), cols = std::min(CB, nc - cb * CB);
-        const int rend = std::min(nr, (rb + 1) * RB);
-        const int rb0 = (cb * CB) / RB;
-        F.rb = B.rb = rb; F.cb = B.cb = cb; F.rows = B.rows = rows; F.cols = B.cols = cols;
-        F.part = vfp[g] + (int64_t)cb * nr + (int64_t)rb * RB;
-        F.comb = vfp[g] + (int64_t)rb * RB;
-        F.cnt = vrbc[g] + rb;
-        F.ntl = std::min(vncb[g], (rend + CB - 1) / CB);
-        set_vec(F, vvo[g] + (int64_t)cb * CB, vvo[g] + (int64_t)cb * CB + cols);
-        B.part = vbp[g] + (int64_t)rb * nc + (int64_t)cb * CB;
-        B.comb = vbp[g] + (int64_t)rb0 * nc + (int64_t)cb * CB;
-        B.cnt = vcbc[g] + cb;
-        B.ntl = vnrb[g] - rb0;
-        set_vec(B, vvo[g] + (int64_t)rb * RB, vvo[g] + (int64_t)rb * RB + rows);
-      }
-      mtf.push_back(F);
-      mtb.push_back(B);
-    }
+    lev[fp.nlevels] = (int)out.size();
   }
-  mt_lev[fp.nlevels] = (int)mtf.size();
   std::vector<int4> ph;
   int nm = 0;
   for (int l = 0; l < fp.nlevels; ++l) {
     ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
-    ph.push_back(make_int4(dev::PH_MF, mt_lev[l], mt_lev[l + 1], nm++));
+    ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], nm++));
   }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
     ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
-    ph.push_back(make_int4(dev::PH_MB, mt_lev[l], mt_lev[l + 1], nm++));
+    ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], nm++));
   }
   nphases_noprolong = (int)ph.size();
   if (prolong_n > 0) {
@@ -261,7 +301,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   if (getenv("MDD_PLAN_STATS")) {
     int nbig = 0;
-    for (int g = 0; g < nsn; ++g) nbig += !small[g];
+    for (int g = 0; g < nsn; ++g) nbig += mode[g] != 0;
     fprintf(stderr, "[mdd plan %s] nsn %d (big %d) levels %d entries %lld tiles %d (%.1f%% stored) mtasks %d "
             "rows %lld contrib %lld grid %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(),
             ntiles, 100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), (int)mtf.size(),
@@ -272,11 +312,11 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         ent += (long long)fp.sn_ncol[g] * (fp.sn_ncol[g] + fp.sn_noff[g]);
-        big += !small[g];
+        big += mode[g] != 0;
       }
       fprintf(stderr, "  level %2d: sn %6d (big %4d) stored %10lld rows %8lld mtasks %6d\n", l,
               fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, (long long)(lev_row[l + 1] - lev_row[l]),
-              mt_lev[l + 1] - mt_lev[l]);
+              lev_f[l + 1] - lev_f[l]);
     }
   }
 }

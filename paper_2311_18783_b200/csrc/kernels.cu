@@ -318,6 +318,51 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
   if (part) block_sum_store(contrib, part);
 }
 
+// y = M x with TPR lanes per row (rows grid-strided over a fixed, SM-sized grid);
+// optional fused partial dot(dotw, y) per block into part[blockIdx.x]
+template <int TPR>
+__device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict__ ptr,
+                                                const int32_t* __restrict__ idx,
+                                                const double* __restrict__ val,
+                                                const double* __restrict__ x, double* __restrict__ y,
+                                                const double* __restrict__ dotw, double* __restrict__ part,
+                                                const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) / TPR;
+  const int lane = threadIdx.x & (TPR - 1);
+  const int ngroups = gridDim.x * blockDim.x / TPR;
+  double dsum = 0.0;
+  for (int row = g; row < nrows; row += ngroups) {
+    const int64_t a = ptr[row], b = ptr[row + 1];
+    double s0 = 0.0, s1 = 0.0;
+    int64_t k = a + lane;
+    for (; k + TPR < b; k += 2 * TPR) {
+      s0 += val[k] * x[idx[k]];
+      s1 += val[k + TPR] * x[idx[k + TPR]];
+    }
+    if (k < b) s0 += val[k] * x[idx[k]];
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
+    if (lane == 0) {
+      y[row] = s;
+      if (dotw) dsum += dotw[row] * s;
+    }
+  }
+  if (part) block_sum_store(dsum, part);
+}
+#define MDD_SPMV_G(NAME, TPR)                                                                      \
+  __global__ void __launch_bounds__(256)                                                           \
+      NAME(int nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,          \
+           const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y, \
+           const double* __restrict__ dotw, double* __restrict__ part, const int* __restrict__ stop) { \
+    spmv_g_body<TPR>(nrows, ptr, idx, val, x, y, dotw, part, stop);                               \
+  }
+MDD_SPMV_G(k_spmv8, 8)
+MDD_SPMV_G(k_spmv16, 16)
+MDD_SPMV_G(k_spmv32, 32)
+#undef MDD_SPMV_G
+
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ part, const int* __restrict__ stop) {
   if (STOPPED) return;

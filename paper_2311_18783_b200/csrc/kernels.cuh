@@ -107,7 +107,7 @@ struct __align__(16) MTaskDesc {
   long long part;   // big: offset of this tile's partial sums (fpart / bpart)
   long long comb;   // big: first partial of the combine (row block / column block)
   long long cnt;    // big: index of the row-block / column-block counter
-  int big, k0, k1;  // small / big tile; tdesc range
+  int big, k0, k1;  // 0 small / 1 big 2-D tile / 2 strip (rb, cb = first row / column); tdesc range
   int nr, nc, rows, cols, rb, cb, RB, CB;
   int ntl;          // big: tiles combined by the last arriver
   int voff;         // offset of the vector inside its shared-memory buffer
@@ -172,6 +172,16 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
                        const double* __restrict__ val, const double* __restrict__ x,
                        double* __restrict__ y, const double* __restrict__ dotw,
                        double* __restrict__ part, const int* __restrict__ stop);
+// y = M x, 8 / 16 / 32 lanes per row on an SM-sized grid, optional fused dot partials
+#define MDD_SPMV_G_DECL(NAME)                                                                    \
+  __global__ void NAME(int nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx, \
+                       const double* __restrict__ val, const double* __restrict__ x,                \
+                       double* __restrict__ y, const double* __restrict__ dotw,                     \
+                       double* __restrict__ part, const int* __restrict__ stop);
+MDD_SPMV_G_DECL(k_spmv8)
+MDD_SPMV_G_DECL(k_spmv16)
+MDD_SPMV_G_DECL(k_spmv32)
+#undef MDD_SPMV_G_DECL
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ part, const int* __restrict__ stop);
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,

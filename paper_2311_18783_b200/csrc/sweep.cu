@@ -54,16 +54,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* m) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
 }
-// one thread: arm the barrier for `bytes` and start the bulk copy global -> shared
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(m))
-      : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -101,22 +91,6 @@ __device__ void grid_barrier(unsigned long long* ctl, unsigned long long target)
   __syncthreads();
 }
 
-struct TileGeo {
-  int nr, nc, RB, CB, nrb, ncb, rows, cols;
-};
-__device__ __forceinline__ TileGeo geo(const SweepDev& S, int g, int rb, int cb) {
-  TileGeo t;
-  t.nc = S.P.sn_ncol[g];
-  t.nr = t.nc + S.P.sn_noff[g];
-  t.RB = S.sn_RB[g];
-  t.CB = S.sn_CB[g];
-  t.nrb = S.sn_nrb[g];
-  t.ncb = S.sn_ncb[g];
-  t.rows = min(t.RB, t.nr - rb * t.RB);
-  t.cols = min(t.CB, t.nc - cb * t.CB);
-  return t;
-}
-
 // y_i = sum_j T[j*R + i] v[j] for i < R (T col-major in smem); fin(i, y_i) is called
 // once per row by one thread.  Fixed-order reduction over column slices.
 template <class Fin>
@@ -136,7 +110,8 @@ __device__ __forceinline__ void tile_matvec(const double* T, int R, int C, const
     }
     return;
   }
-  const int Rp = (R + 31) & ~31;
+  // rows per slice group: a multiple of 32, or a power of two below 32
+  const int Rp = R >= 32 ? (R + 31) & ~31 : (R > 16 ? 32 : R > 8 ? 16 : R > 4 ? 8 : R > 2 ? 4 : R);
   const int nsl = min(kSweepThreads / Rp, C);
   const int i = tid % Rp, sl = tid / Rp;
   if (sl < nsl && i < R) {
@@ -184,10 +159,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   double* const vec2 = vbuf1 + kVecMax + 2;   // kVecMax: accumulators
   double* const red = vec2 + kVecMax;         // kSweepThreads
   __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ int s_next[2];
   __shared__ int s_flag;
   const int tid = threadIdx.x;
-  const PlanDev& P = S.P;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
   const unsigned long long grid = gridDim.x;
@@ -283,7 +256,26 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           if (buf) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
           else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
         };
-        if (!D.big) {
+        if (D.big == 2) {
+          // ---------------- strip of a wide supernode (nr <= kVecMax): fwd = rows
+          // [r0, r0+rows) x all columns, bwd = all rows x columns [c0, c0+cols);
+          // the task vector is the whole t (fwd) / w (bwd): no partial sums
+          next_tile_and_wait(D.k0);
+          const double* T = sm + buf * kTileMax;
+          if (fwd) {
+            double* const upd = S.upd + D.uptr;
+            tile_matvec(T, D.rows, D.nc, vv, red, [&](int i2, double y) {
+              const int r = D.rb + i2;
+              if (r < D.nc) S.xf[D.col0 + r] = y;
+              else upd[r - D.nc] = vv[r] - y;
+            });
+          } else {
+            double* const xb = S.xb + D.col0 + D.cb;
+            tile_matvec_t(T, D.nr, D.cols, vv, [&](int j, double y) { xb[j] = y; });
+          }
+          __syncthreads();
+          buf ^= 1;
+        } else if (!D.big) {
           // ---------------- small supernode: all column tiles, one CTA
           for (int kk = D.k0; kk < D.k1; ++kk) {
             const int cb = kk - D.k0;
@@ -366,21 +358,33 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   }
 }
 
-// relayout of the column-major panels into contiguous tiles (setup)
+// relayout of the column-major panels into contiguous tiles (setup).  tiles[k] =
+// {g, a, b, kind}: 0 2-D (rb, cb), 1 forward row strip (first row a, all columns),
+// 2 backward column strip (all rows, first column b), 3 small column tile (b)
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,
                                 const int64_t* __restrict__ lptr) {
   const int k = blockIdx.x;
   if (k >= ntiles) return;
   const int4 tl = S.tiles[k];
-  const int g = tl.x, rb = tl.y, cb = tl.z;
-  const TileGeo G = geo(S, g, rb, cb);
-  const double* src = L + lptr[g] + (i64)(cb * G.CB) * G.nr + rb * G.RB;
-  double* dst = const_cast<double*>(S.Lt) + S.tile_off[k];
-  for (int q = threadIdx.x; q < G.rows * G.cols; q += blockDim.x) {
-    const int j = q / G.rows, i = q % G.rows;
-    dst[q] = src[(i64)j * G.nr + i];
+  const int g = tl.x, kind = tl.w;
+  const int nc = S.P.sn_ncol[g], nr = nc + S.P.sn_noff[g];
+  const int RB = S.sn_RB[g], CB = S.sn_CB[g];
+  int r0 = 0, c0 = 0, rows = nr, cols = nc;
+  if (kind == 0) {
+    r0 = tl.y * RB; c0 = tl.z * CB;
+    rows = min(RB, nr - r0); cols = min(CB, nc - c0);
+  } else if (kind == 1) {
+    r0 = tl.y; rows = min(RB, nr - r0);
+  } else {
+    c0 = tl.z; cols = min(CB, nc - c0);
   }
-  if (threadIdx.x == 0 && ((G.rows * G.cols) & 1)) dst[G.rows * G.cols] = 0.0;
+  const double* src = L + lptr[g] + (i64)c0 * nr + r0;
+  double* dst = const_cast<double*>(S.Lt) + S.tile_off[k];
+  for (int q = threadIdx.x; q < rows * cols; q += blockDim.x) {
+    const int j = q / rows, i = q % rows;
+    dst[q] = src[(i64)j * nr + i];
+  }
+  if (threadIdx.x == 0 && ((rows * cols) & 1)) dst[rows * cols] = 0.0;
 }
 
 }  // namespace dev
