@@ -332,19 +332,24 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
   const int lane = threadIdx.x & (TPR - 1);
   const int ngroups = gridDim.x * blockDim.x / TPR;
   double dsum = 0.0;
-  for (int row = g; row < nrows; row += ngroups) {
-    const int64_t a = ptr[row], b = ptr[row + 1];
+  // the trip count is uniform per warp (the shuffles need every lane of the warp)
+  for (int row = g;; row += ngroups) {
+    const bool active = row < nrows;
+    if (!__any_sync(0xffffffffu, active)) break;
     double s0 = 0.0, s1 = 0.0;
-    int64_t k = a + lane;
-    for (; k + TPR < b; k += 2 * TPR) {
-      s0 += val[k] * x[idx[k]];
-      s1 += val[k + TPR] * x[idx[k + TPR]];
+    if (active) {
+      const int64_t a = ptr[row], b = ptr[row + 1];
+      int64_t k = a + lane;
+      for (; k + TPR < b; k += 2 * TPR) {
+        s0 += val[k] * x[idx[k]];
+        s1 += val[k + TPR] * x[idx[k + TPR]];
+      }
+      if (k < b) s0 += val[k] * x[idx[k]];
     }
-    if (k < b) s0 += val[k] * x[idx[k]];
     double s = s0 + s1;
 #pragma unroll
     for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
-    if (lane == 0) {
+    if (active && lane == 0) {
       y[row] = s;
       if (dotw) dsum += dotw[row] * s;
     }
