@@ -136,6 +136,8 @@ enum {
   MDD_INFO_LAST_LAUNCHES,   /* kernels launched by the last solve/apply call */
   MDD_INFO_COARSE_PERTURBED,/* pivots of the Jacobi-scaled E raised to the static-pivot
                                threshold 1e-14 (kappa(E) ~ 1/eps; 0 = exact LDL^T)   */
+  MDD_INFO_NNZ_ZG,          /* entries of the gradient (SNK / NK) part of Z        */
+  MDD_INFO_NNZ_W,           /* entries of the dense GenEO blocks of Z              */
   MDD_INFO_COUNT
 };
 int mdd_info(mdd_handle h, int64_t* out, int count);

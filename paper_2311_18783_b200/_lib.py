@@ -21,7 +21,7 @@ INFO_NAMES = ["n", "nedges", "nfree_nodes", "nsub", "nnz_A", "nloc", "grad_candi
               "grad_rank", "ngeneo", "n0", "local_factor_nnz", "coarse_factor_nnz",
               "local_supernodes", "local_levels", "coarse_supernodes", "coarse_levels",
               "nnz_Z", "kernels_per_iter", "last_launches",
-              "coarse_perturbed"]
+              "coarse_perturbed", "nnz_Zg", "nnz_W"]
 INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, "A_ptr": 4,
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
               "geneo_count": 10}

@@ -189,9 +189,17 @@ struct mdd_solver {
   // coarse
   bool has_coarse = false;
   DevFactor crs;
-  DBuf<int64_t> Z_ptr, Zt_ptr;  // Z: n x n0 (cols = coarse positions); Zt: n0 x n
+  DBuf<int64_t> Z_ptr, Zt_ptr;  // setup only: mixed Z (n x n0, cols = coarse positions), Z^T
   DBuf<int32_t> Z_idx, Zt_idx;
   DBuf<double> Z_val, Zt_val;
+  // hot path: gradient part of Z (CSR by dof and by coarse position) + dense GenEO blocks
+  DBuf<int64_t> Zg_ptr, Zgt_ptr, W_off, W_poff;
+  DBuf<int32_t> Zg_idx, Zgt_idx, W_gpos;
+  DBuf<double> Zg_val, Zgt_val, W_val, u_loc;
+  DBuf<int> W_n, W_k, W_gc0;
+  DBuf<int4> W_bzt, W_bz;
+  int nbzt = 0, nbz = 0;
+  int64_t nnzZg = 0, nnzW = 0;
   int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0, coarse_perturbed = 0;
   std::vector<int64_t> geneo_count;
   std::vector<double> geneo_lambda;
@@ -249,13 +257,21 @@ struct mdd_solver {
     loc.sweep(rr, zz, stream, state.p);
     launches += 1;
   }
+  // y = Z E^{-1} Z^T v: Z_g^T v (CSR) and Z_e^T v (tall-skinny over the GenEO blocks),
+  // the sweep on E, then Z_g xc + prolongation of the GenEO blocks' W_i xc_i
   void apply_coarse(const double* v, double* y) {
-    dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zt_ptr.p, Zt_idx.p, Zt_val.p, v, xc.p,
-                                                   nullptr, nullptr, state.p);
+    dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, xc.p,
+                                              nullptr, nullptr, state.p);
+    if (nbzt)
+      dev::k_geneo_zt<<<nbzt, 256, 0, stream>>>(W_bzt.p, W_off.p, W_poff.p, W_n.p, W_gc0.p, W_gpos.p, W_val.p,
+                                                gmap.p, v, xc.p, state.p);
     crs.sweep(xc.p, nullptr, stream, state.p);
-    dev::k_spmv16<<<nparts, 256, 0, stream>>>(n, Z_ptr.p, Z_idx.p, Z_val.p, crs.xb.p, y, nullptr,
-                                                   nullptr, state.p);
-    launches += 3;
+    if (nbz)
+      dev::k_geneo_z<<<nbz, 256, 0, stream>>>(W_bz.p, W_off.p, W_poff.p, W_n.p, W_k.p, W_gc0.p, W_gpos.p,
+                                              W_val.p, crs.xb.p, u_loc.p, state.p);
+    dev::k_z_apply<<<nparts, 256, 0, stream>>>(n, Zg_ptr.p, Zg_idx.p, Zg_val.p, crs.xb.p, pro_ptr.p, pro_pos.p,
+                                              nbz ? u_loc.p : nullptr, y, state.p);
+    launches += 3 + (nbzt ? 1 : 0) + (nbz ? 1 : 0);
   }
   void apply_prec(const double* rr, double* zz) {
     int v = desc.variant;
@@ -761,6 +777,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       CUDA_CHECK(cudaMemcpy(zi.data(), Z.idx.p, Z.nnz * sizeof(int), cudaMemcpyDeviceToHost));
       std::vector<int64_t> zp64(n + 1);
       for (int e = 0; e <= n; ++e) zp64[e] = zp[e];
+      std::vector<int> zi_orig = zi;
       for (auto& c : zi) c = H->crs.fp.iperm_global[c];
       H->Z_ptr.upload(zp64);
       H->Z_idx.upload(zi);
@@ -793,6 +810,82 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       dsrc.upload(src);
       dev::k_gather<<<nblk(Zt.nnz, 256), 256, 0, s>>>(Zt.nnz, dsrc.p, Zt.val.p, H->Zt_val.p);
       CUDA_CHECK(cudaStreamSynchronize(s));
+      // ---- hot path: gradient part of Z as CSR (both orientations), GenEO part as
+      // dense n_i x k_i blocks in the local solves' position order, so Z_e^T v is a
+      // tall-skinny reduction and Z_e y a dense mat-vec plus the prolongation
+      const int64_t gr = H->grad_rank;
+      {
+        std::vector<int64_t> gp(n + 1, 0), gsrc;
+        std::vector<int32_t> gi;
+        for (int e = 0; e < n; ++e) {
+          for (int k = zp[e]; k < zp[e + 1]; ++k)
+            if (zi_orig[k] < gr) { gi.push_back(zi[k]); gsrc.push_back(k); }
+          gp[e + 1] = (int64_t)gi.size();
+        }
+        H->nnzZg = (int64_t)gi.size();
+        H->Zg_ptr.upload(gp);
+        H->Zg_idx.upload(gi.empty() ? std::vector<int32_t>{0} : gi);
+        H->Zg_val.alloc(std::max<int64_t>(H->nnzZg, 1));
+        DBuf<int64_t> d2;
+        d2.upload(gsrc.empty() ? std::vector<int64_t>{0} : gsrc);
+        if (H->nnzZg)
+          dev::k_gather<<<nblk(H->nnzZg, 256), 256, 0, s>>>(H->nnzZg, d2.p, H->Z_val.p, H->Zg_val.p);
+        // Z_g^T: the GenEO positions get empty rows (k_geneo_zt writes them)
+        std::vector<int64_t> tp2(nb + 1, 0), tsrc;
+        std::vector<int32_t> ti2;
+        for (int64_t pidx = 0; pidx < nb; ++pidx) {
+          if (col_of_pos[pidx] < gr)
+            for (int64_t k = ptr2[pidx]; k < ptr2[pidx + 1]; ++k) { ti2.push_back(idx2[k]); tsrc.push_back(k); }
+          tp2[pidx + 1] = (int64_t)ti2.size();
+        }
+        H->Zgt_ptr.upload(tp2);
+        H->Zgt_idx.upload(ti2.empty() ? std::vector<int32_t>{0} : ti2);
+        H->Zgt_val.alloc(std::max<int64_t>((int64_t)ti2.size(), 1));
+        DBuf<int64_t> d3;
+        d3.upload(tsrc.empty() ? std::vector<int64_t>{0} : tsrc);
+        if (!ti2.empty())
+          dev::k_gather<<<nblk((int64_t)ti2.size(), 256), 256, 0, s>>>((int64_t)ti2.size(), d3.p, H->Zt_val.p,
+                                                                     H->Zgt_val.p);
+        CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+      if (H->ngeneo > 0) {
+        const FactorPlan& lp = H->loc.fp;
+        std::vector<int64_t> woff(nsub, 0), poff(nsub, 0), wsrc;
+        std::vector<int> nsz(nsub), kc(nsub), gc0(nsub);
+        std::vector<int32_t> gpos(H->ngeneo);
+        std::vector<int4> bzt, bz;
+        int64_t wtot = 0;
+        int gcol = 0;
+        for (int i = 0; i < nsub; ++i) {
+          const int ni = (int)H->dec.sub_dofs[i].size(), ki = geneo[i].k;
+          nsz[i] = ni; kc[i] = ki; gc0[i] = gcol; woff[i] = wtot; poff[i] = lp.sys_off[i];
+          for (int k = 0; k < ki; ++k) {
+            const int64_t c = gr + gcol + k;  // original coarse column
+            gpos[gcol + k] = H->crs.fp.iperm_global[c];
+            MDD_REQUIRE(tp[c + 1] - tp[c] == ni, 5, "GenEO column is not dense on its subdomain");
+            for (int q = 0; q < ni; ++q) wsrc.push_back(tp[c] + lp.perm[lp.sys_off[i] + q]);
+          }
+          for (int k0 = 0; k0 < ki; k0 += 8) bzt.push_back(make_int4(i, k0, std::min(8, ki - k0), 0));
+          if (ki > 0)
+            for (int r0 = 0; r0 < ni; r0 += 256) bz.push_back(make_int4(i, r0, 0, 0));
+          wtot += (int64_t)ni * ki;
+          gcol += ki;
+        }
+        H->nnzW = wtot;
+        H->W_val.alloc(wtot);
+        DBuf<int64_t> d4;
+        d4.upload(wsrc);
+        dev::k_gather<<<nblk(wtot, 256), 256, 0, s>>>(wtot, d4.p, Zt.val.p, H->W_val.p);
+        H->W_off.upload(woff); H->W_poff.upload(poff); H->W_n.upload(nsz); H->W_k.upload(kc);
+        H->W_gc0.upload(gc0); H->W_gpos.upload(gpos); H->W_bzt.upload(bzt); H->W_bz.upload(bz);
+        H->nbzt = (int)bzt.size();
+        H->nbz = (int)bz.size();
+        H->u_loc.alloc(lp.ntot);
+        CUDA_CHECK(cudaStreamSynchronize(s));
+      }
+      // the mixed CSR copies are not needed on the hot path
+      H->Z_ptr.release(); H->Z_idx.release(); H->Z_val.release();
+      H->Zt_ptr.release(); H->Zt_idx.release(); H->Zt_val.release();
     }
     H->setup_times[PH_COARSE_FACTOR] = now_s() - t0;
   }
@@ -1011,6 +1104,8 @@ int mdd_info(mdd_handle h, int64_t* out, int count) {
   v[MDD_INFO_KERNELS_PER_ITER] = 0;
   v[MDD_INFO_LAST_LAUNCHES] = h->launches;
   v[MDD_INFO_COARSE_PERTURBED] = h->coarse_perturbed;
+  v[MDD_INFO_NNZ_ZG] = h->nnzZg;
+  v[MDD_INFO_NNZ_W] = h->nnzW;
   for (int k = 0; k < count && k < MDD_INFO_COUNT; ++k) out[k] = v[k];
   return MDD_OK;
 }

@@ -368,6 +368,83 @@ MDD_SPMV_G(k_spmv16, 16)
 MDD_SPMV_G(k_spmv32, 32)
 #undef MDD_SPMV_G
 
+// ---------------------------------------------------------- GenEO blocks
+// Z_e^T v: y[gpos[c]] = sum_p W_i[p + k n_i] v[gmap[off_i + p]] for the GenEO
+// columns k of subdomain i (tall-skinny reduction, fixed order: per thread a
+// strided row range, then warp shuffles, then the warps in order)
+__global__ void __launch_bounds__(256) k_geneo_zt(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
+                                                  const int64_t* __restrict__ poff, const int* __restrict__ nsz,
+                                                  const int* __restrict__ gcol0, const int32_t* __restrict__ gpos,
+                                                  const double* __restrict__ W, const int32_t* __restrict__ gmap,
+                                                  const double* __restrict__ v, double* __restrict__ y,
+                                                  const int* __restrict__ stop) {
+  if (STOPPED) return;
+  constexpr int KC = 8;
+  __shared__ double red[8][KC];
+  const int4 b = blk[blockIdx.x];  // {subdomain, first column, columns, -}
+  const int i = b.x, k0 = b.y, kc = b.z;
+  const int ni = nsz[i];
+  const double* Wi = W + woff[i] + (int64_t)k0 * ni;
+  const int32_t* gm = gmap + poff[i];
+  double acc[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) acc[q] = 0.0;
+  for (int p = threadIdx.x; p < ni; p += blockDim.x) {
+    const double vp = v[gm[p]];
+#pragma unroll
+    for (int q = 0; q < KC; ++q)
+      if (q < kc) acc[q] += Wi[(int64_t)q * ni + p] * vp;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < KC; ++q) {
+    const double t = warp_sum(acc[q]);
+    if (lane == 0) red[w][q] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < kc) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q][threadIdx.x];
+    y[gpos[gcol0[i] + k0 + threadIdx.x]] = t;
+  }
+}
+
+// u[off_i + p] = sum_k W_i[p + k n_i] xc[gpos[gcol0_i + k]]  (rows of subdomain i)
+__global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
+                                                 const int64_t* __restrict__ poff, const int* __restrict__ nsz,
+                                                 const int* __restrict__ kcnt, const int* __restrict__ gcol0,
+                                                 const int32_t* __restrict__ gpos, const double* __restrict__ W,
+                                                 const double* __restrict__ xc, double* __restrict__ u,
+                                                 const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const int4 b = blk[blockIdx.x];  // {subdomain, first row, -, -}
+  const int i = b.x;
+  const int ni = nsz[i], ki = kcnt[i];
+  const int p = b.y + threadIdx.x;
+  if (p >= ni) return;
+  const double* Wi = W + woff[i];
+  const int32_t* gp = gpos + gcol0[i];
+  double s = 0.0;
+  for (int k = 0; k < ki; ++k) s += Wi[(int64_t)k * ni + p] * xc[gp[k]];
+  u[poff[i] + p] = s;
+}
+
+// out[e] = Z_g(e, :) xc + sum of the GenEO contributions u at the copies of e
+__global__ void __launch_bounds__(256) k_z_apply(int n, const int64_t* __restrict__ ptr,
+                                                 const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                                 const double* __restrict__ xc, const int64_t* __restrict__ pptr,
+                                                 const int32_t* __restrict__ ppos, const double* __restrict__ u,
+                                                 double* __restrict__ out, const int* __restrict__ stop) {
+  if (STOPPED) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = ptr[e]; k < ptr[e + 1]; ++k) s += val[k] * xc[idx[k]];
+    if (u)
+      for (int64_t k = pptr[e]; k < pptr[e + 1]; ++k) s += u[ppos[k]];
+    out[e] = s;
+  }
+}
+
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ part, const int* __restrict__ stop) {
   if (STOPPED) return;

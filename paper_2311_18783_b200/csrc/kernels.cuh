@@ -182,6 +182,20 @@ MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
 MDD_SPMV_G_DECL(k_spmv32)
 #undef MDD_SPMV_G_DECL
+__global__ void k_geneo_zt(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
+                           const int64_t* __restrict__ poff, const int* __restrict__ nsz,
+                           const int* __restrict__ gcol0, const int32_t* __restrict__ gpos,
+                           const double* __restrict__ W, const int32_t* __restrict__ gmap,
+                           const double* __restrict__ v, double* __restrict__ y, const int* __restrict__ stop);
+__global__ void k_geneo_z(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
+                          const int64_t* __restrict__ poff, const int* __restrict__ nsz,
+                          const int* __restrict__ kcnt, const int* __restrict__ gcol0,
+                          const int32_t* __restrict__ gpos, const double* __restrict__ W,
+                          const double* __restrict__ xc, double* __restrict__ u, const int* __restrict__ stop);
+__global__ void k_z_apply(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                          const double* __restrict__ val, const double* __restrict__ xc,
+                          const int64_t* __restrict__ pptr, const int32_t* __restrict__ ppos,
+                          const double* __restrict__ u, double* __restrict__ out, const int* __restrict__ stop);
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ part, const int* __restrict__ stop);
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,

@@ -151,8 +151,10 @@ class MaxwellDD:
         # local sweep: every factor entry once per direction, D^{-1}, the restriction
         # of r and the prolongated result (the kernel's own scratch is not counted)
         local = 2 * 8 * i["local_factor_nnz"] + 8 * nloc + 8 * n + 8 * n
-        coarse = (2 * 12 * i["nnz_Z"] + 2 * 8 * i["coarse_factor_nnz"] + 8 * i["n0"] + 16 * n) \
-            if i["n0"] else 0
+        # coarse: gradient part of Z as CSR (12 B / entry) and the dense GenEO blocks
+        # (8 B / entry), each read in Z^T v and in Z y; E's factor in both sweeps
+        coarse = (2 * 12 * i["nnz_Zg"] + 2 * 8 * i["nnz_W"] + 2 * 8 * i["coarse_factor_nnz"]
+                  + 8 * i["n0"] + 16 * n) if i["n0"] else 0
         vec = 8 * n * 4
         precond = local + 2 * coarse + 2 * spmv + vec
         return {"spmv": spmv, "local": local, "coarse": coarse, "precond": precond,
