@@ -8,6 +8,10 @@
 
 namespace mdd {
 
+namespace {
+constexpr int kGroup = 4;  // 2-D tiles per sweep task (accumulated in shared memory)
+}  // namespace
+
 dev::PlanDev DevFactor::plan() const {
   dev::PlanDev P;
   P.sn_col0 = (const long long*)col0.p;
@@ -92,11 +96,11 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       for (int c0 = 0; c0 < nc; c0 += cs) bt[g].push_back(add_tile(make_int4(g, 0, c0, 2), nr, std::min(cs, nc - c0)));
     } else {
       const int CB = std::min(nc, 64);
-      const int RB = std::min(dev::kVecMax, std::max(32, (dev::kTileMax / CB) / 32 * 32));
+      const int RB = std::max(1, dev::kTileMax / CB);
       const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
-      vfp[g] = nfp; nfp += (int64_t)ncb * nr;
-      vbp[g] = nbp; nbp += (int64_t)nrb * nc;
+      vfp[g] = nfp; nfp += (int64_t)((ncb + kGroup - 1) / kGroup) * nr;
+      vbp[g] = nbp; nbp += (int64_t)((nrb + kGroup - 1) / kGroup) * nc;
       vrbc[g] = nrbc; nrbc += nrb;
       vcbc[g] = ncbc; ncbc += ncb;
       for (int rb = 0; rb < nrb; ++rb) {
@@ -160,12 +164,17 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     X.voff = (int)(lo - X.vlo2);
     X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
   };
+  struct Cand {
+    int64_t bytes;
+    dev::MTaskDesc d;
+    std::vector<int> tiles;
+  };
   for (int dir = 0; dir < 2; ++dir) {
     std::vector<dev::MTaskDesc>& out = dir == 0 ? mtf : mtb;
     std::vector<int>& lev = dir == 0 ? lev_f : lev_b;
     for (int l = 0; l < fp.nlevels; ++l) {
       lev[l] = (int)out.size();
-      std::vector<std::pair<int64_t, dev::MTaskDesc>> lt;
+      std::vector<Cand> lt;
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
@@ -176,70 +185,82 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         D.nr = nr; D.nc = nc; D.RB = vRB[g]; D.CB = vCB[g];
         const std::vector<int>& tiles_g = dir == 0 ? ft[g] : bt[g];
         if (mode[g] == 0) {
+          // small: one task, all column tiles
           D.big = 0;
           D.rows = nr; D.cols = nc;
           set_vec(D, vvo[g], vvo[g] + nr);
           int64_t by = 0;
           for (int t : tiles_g) by += tile_bytes(t);
-          D.k0 = -1;
-          D.k1 = (int)tiles_g.size();  // resolved to tdesc ranges below
-          D.part = tiles_g.empty() ? -1 : tiles_g[0];
-          lt.push_back({by, D});
-        } else {
+          lt.push_back({by, D, tiles_g});
+        } else if (mode[g] == 1) {
+          // strip: one task per strip, the whole t / w as vector
           for (int t : tiles_g) {
             dev::MTaskDesc X = D;
-            X.big = mode[g] == 1 ? 2 : 1;
+            X.big = 2;
             X.rows = rc[t].x; X.cols = rc[t].y;
-            X.k0 = -2;
-            X.part = t;  // tile, resolved below
-            if (mode[g] == 1) {
-              X.rb = tl[t].y;
-              X.cb = tl[t].z;
-              set_vec(X, vvo[g], vvo[g] + nr);
-            } else {
-              const int rb = tl[t].y, cb = tl[t].z, RB = vRB[g], CB = vCB[g];
+            X.rb = tl[t].y;
+            X.cb = tl[t].z;
+            set_vec(X, vvo[g], vvo[g] + nr);
+            lt.push_back({tile_bytes(t), X, {t}});
+          }
+        } else {
+          // 2-D: groups of <= kGroup tiles; fwd = one row block x consecutive column
+          // blocks, bwd = one column block x consecutive row blocks
+          const int RB = vRB[g], CB = vCB[g], nrb = vnrb[g], ncb = vncb[g];
+          std::vector<std::vector<int>> tid_of(nrb, std::vector<int>(ncb, -1));
+          for (int t : tiles_g) tid_of[tl[t].y][tl[t].z] = t;
+          if (dir == 0) {
+            for (int rb = 0; rb < nrb; ++rb) {
               const int rend = std::min(nr, (rb + 1) * RB);
-              const int rb0 = (cb * CB) / RB;
-              X.rb = rb; X.cb = cb;
-              if (dir == 0) {
+              const int ntb = std::min(ncb, (rend + CB - 1) / CB);
+              const int nch = (ntb + kGroup - 1) / kGroup;
+              for (int ch = 0; ch < nch; ++ch) {
+                dev::MTaskDesc X = D;
+                X.big = 1;
+                X.rb = rb;
+                X.cb = ch * kGroup;
+                const int cend = std::min(ntb, (ch + 1) * kGroup);
+                X.rows = rend - rb * RB;
+                X.part = vfp[g] + (int64_t)ch * nr + (int64_t)rb * RB;
                 X.comb = vfp[g] + (int64_t)rb * RB;
                 X.cnt = vrbc[g] + rb;
-                X.ntl = std::min(vncb[g], (rend + CB - 1) / CB);
-                set_vec(X, vvo[g] + (int64_t)cb * CB, vvo[g] + (int64_t)cb * CB + X.cols);
-              } else {
-                X.comb = vbp[g] + (int64_t)rb0 * nc + (int64_t)cb * CB;
-                X.cnt = vcbc[g] + cb;
-                X.ntl = vnrb[g] - rb0;
-                set_vec(X, vvo[g] + (int64_t)rb * RB, vvo[g] + (int64_t)rb * RB + X.rows);
+                X.ntl = nch;
+                set_vec(X, vvo[g] + (int64_t)X.cb * CB, vvo[g] + std::min<int64_t>(nc, (int64_t)cend * CB));
+                Cand c{0, X, {}};
+                for (int cb = X.cb; cb < cend; ++cb) { c.tiles.push_back(tid_of[rb][cb]); c.bytes += tile_bytes(tid_of[rb][cb]); }
+                lt.push_back(c);
               }
             }
-            lt.push_back({tile_bytes(t), X});
+          } else {
+            for (int cb = 0; cb < ncb; ++cb) {
+              const int rb0 = (cb * CB) / RB;
+              const int nch = (nrb - rb0 + kGroup - 1) / kGroup;
+              for (int ch = 0; ch < nch; ++ch) {
+                dev::MTaskDesc X = D;
+                X.big = 1;
+                X.cb = cb;
+                X.rb = rb0 + ch * kGroup;
+                const int rend_b = std::min(nrb, X.rb + kGroup);
+                X.cols = std::min(CB, nc - cb * CB);
+                X.part = vbp[g] + (int64_t)ch * nc + (int64_t)cb * CB;
+                X.comb = vbp[g] + (int64_t)cb * CB;
+                X.cnt = vcbc[g] + cb;
+                X.ntl = nch;
+                set_vec(X, vvo[g] + (int64_t)X.rb * RB, vvo[g] + std::min<int64_t>(nr, (int64_t)rend_b * RB));
+                Cand c{0, X, {}};
+                for (int rb = X.rb; rb < rend_b; ++rb) { c.tiles.push_back(tid_of[rb][cb]); c.bytes += tile_bytes(tid_of[rb][cb]); }
+                lt.push_back(c);
+              }
+            }
           }
         }
       }
-      std::stable_sort(lt.begin(), lt.end(), [](const std::pair<int64_t, dev::MTaskDesc>& x,
-                                                const std::pair<int64_t, dev::MTaskDesc>& y) { return x.first > y.first; });
-      for (auto& e : lt) {
-        dev::MTaskDesc X = e.second;
-        const int g = tl[(int)X.part].x;
-        if (X.k0 == -1) {  // small: all its column tiles
-          X.k0 = (int)td.size();
-          for (int t : (dir == 0 ? ft[g] : bt[g])) push_td(t);
-          X.k1 = (int)td.size();
-          X.part = 0;
-        } else {
-          const int t = (int)X.part;
-          X.k0 = (int)td.size();
-          push_td(t);
-          X.k1 = (int)td.size();
-          if (X.big == 1) {
-            const int nr = X.nr, nc = X.nc;
-            X.part = dir == 0 ? vfp[g] + (int64_t)X.cb * nr + (int64_t)X.rb * X.RB
-                              : vbp[g] + (int64_t)X.rb * nc + (int64_t)X.cb * X.CB;
-          } else {
-            X.part = 0;
-          }
-        }
+      std::stable_sort(lt.begin(), lt.end(), [](const Cand& x, const Cand& y) { return x.bytes > y.bytes; });
+      for (auto& c : lt) {
+        dev::MTaskDesc X = c.d;
+        X.k0 = (int)td.size();
+        for (int t : c.tiles) push_td(t);
+        X.k1 = (int)td.size();
         out.push_back(X);
       }
     }

@@ -302,19 +302,39 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             }
           }
         } else {
-          // ---------------- one tile of a big supernode
-          next_tile_and_wait(D.k0);
-          const double* T = sm + buf * kTileMax;
-          double* const part = (fwd ? S.fpart : S.bpart) + D.part;
-          if (fwd) tile_matvec(T, D.rows, D.cols, vv, red, [&](int r, double y) { part[r] = y; });
-          else tile_matvec_t(T, D.rows, D.cols, vv, [&](int j, double y) { part[j] = y; });
+          // ---------------- a group of <= 4 tiles of a 2-D supernode: one row block and
+          // consecutive column blocks (fwd) / one column block and consecutive row
+          // blocks (bwd), accumulated in shared memory into one partial sum
+          for (int kk = D.k0; kk < D.k1; ++kk) {
+            const int j = kk - D.k0;
+            next_tile_and_wait(kk);
+            const double* T = sm + buf * kTileMax;
+            if (fwd) {
+              const int cols = min(D.CB, D.nc - (D.cb + j) * D.CB);
+              if (j == 0) tile_matvec(T, D.rows, cols, vv, red, [&](int r, double y) { vec2[r] = y; });
+              else tile_matvec(T, D.rows, cols, vv + j * D.CB, red, [&](int r, double y) { vec2[r] += y; });
+            } else {
+              const int rows = min(D.RB, D.nr - (D.rb + j) * D.RB);
+              if (j == 0) tile_matvec_t(T, rows, D.cols, vv, [&](int c, double y) { vec2[c] = y; });
+              else tile_matvec_t(T, rows, D.cols, vv + j * D.RB, [&](int c, double y) { vec2[c] += y; });
+            }
+            __syncthreads();
+            buf ^= 1;
+          }
+          {
+            double* const part = (fwd ? S.fpart : S.bpart) + D.part;
+            const int m = fwd ? D.rows : D.cols;
+            for (int q = tid; q < m; q += kSweepThreads) part[q] = vec2[q];
+          }
           __syncthreads();
-          buf ^= 1;
           if (tid == 0) {
-            __threadfence();
+            // one acq_rel atomic publishes this group's partial sums and tells the
+            // last group of the row / column block to combine
             unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
-            s_flag = atomicAdd(c, 1ull) + 1 == cur * (unsigned long long)D.ntl;
+            unsigned long long old;
             __threadfence();
+            asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(c) : "memory");
+            s_flag = old + 1 == cur * (unsigned long long)D.ntl;
           }
           __syncthreads();
           if (s_flag) {
