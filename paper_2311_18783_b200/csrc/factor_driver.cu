@@ -8,9 +8,6 @@
 
 namespace mdd {
 
-namespace {
-constexpr int kGroup = 4;  // 2-D tiles per sweep task (accumulated in shared memory)
-}  // namespace
 
 dev::PlanDev DevFactor::plan() const {
   dev::PlanDev P;
@@ -99,8 +96,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       const int RB = std::max(1, dev::kTileMax / CB);
       const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
-      vfp[g] = nfp; nfp += (int64_t)((ncb + kGroup - 1) / kGroup) * nr;
-      vbp[g] = nbp; nbp += (int64_t)((nrb + kGroup - 1) / kGroup) * nc;
+      vfp[g] = nfp; nfp += (int64_t)ncb * nr;   // sized for groups of one tile
+      vbp[g] = nbp; nbp += (int64_t)nrb * nc;
       vrbc[g] = nrbc; nrbc += nrb;
       vcbc[g] = ncbc; ncbc += ncb;
       for (int rb = 0; rb < nrb; ++rb) {
@@ -169,12 +166,29 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     dev::MTaskDesc d;
     std::vector<int> tiles;
   };
+  // persistent grid (needed to size the 2-D tile groups)
+  const int smem = dev::kSweepSmemDoubles * (int)sizeof(double);
+  CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  {
+    int dev_id = 0, nsm = 0, per_sm = 0;
+    CUDA_CHECK(cudaGetDevice(&dev_id));
+    CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
+    MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
+    sweep_grid = nsm * per_sm;
+  }
   for (int dir = 0; dir < 2; ++dir) {
     std::vector<dev::MTaskDesc>& out = dir == 0 ? mtf : mtb;
     std::vector<int>& lev = dir == 0 ? lev_f : lev_b;
     for (int l = 0; l < fp.nlevels; ++l) {
       lev[l] = (int)out.size();
       std::vector<Cand> lt;
+      // 2-D tiles per task: fewer, larger tasks only while they still cover the
+      // grid twice over (a level with few tiles is latency-bound)
+      int64_t t2d = 0;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k)
+        if (mode[fp.level_sn[k]] == 2) t2d += (int64_t)(dir == 0 ? ft : bt)[fp.level_sn[k]].size();
+      const int kGroup = t2d >= (int64_t)8 * sweep_grid ? 4 : (t2d >= (int64_t)4 * sweep_grid ? 2 : 1);
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
@@ -308,14 +322,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   ctl.alloc(dev::SW_COUNT);
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
-  const int smem = dev::kSweepSmemDoubles * (int)sizeof(double);
-  CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int dev_id = 0, nsm = 0, per_sm = 0;
-  CUDA_CHECK(cudaGetDevice(&dev_id));
-  CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
-  CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
-  MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
-  sweep_grid = nsm * per_sm;
   if (getenv("MDD_SWEEP_TRACE")) {
     trace.alloc((size_t)2 * nphases * sweep_grid);
     CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
