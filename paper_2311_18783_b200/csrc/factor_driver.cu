@@ -188,7 +188,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       int64_t t2d = 0;
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k)
         if (mode[fp.level_sn[k]] == 2) t2d += (int64_t)(dir == 0 ? ft : bt)[fp.level_sn[k]].size();
-      const int kGroup = t2d >= (int64_t)8 * sweep_grid ? 4 : (t2d >= (int64_t)4 * sweep_grid ? 2 : 1);
+      (void)t2d;
+      const int kGroup = 4;
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];

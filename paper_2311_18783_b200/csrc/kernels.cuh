@@ -96,7 +96,9 @@ constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 3840;   // doubles per tile (30 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
-constexpr int kSweepSmemDoubles = 2 * kTileMax + 3 * kVecMax + 4 + kSweepThreads;
+constexpr int kStages = 3;       // tile ring slots per CTA (two tiles stream while one computes)
+constexpr int kVecSlots = 4;     // task-vector slots (> the tasks a 3-slot ring can span)
+constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
 
 // one task of an M phase (factor_driver.cu builds them, forward and backward)
 struct __align__(16) MTaskDesc {

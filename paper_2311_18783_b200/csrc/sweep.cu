@@ -152,13 +152,14 @@ __device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, con
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
+__global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepDev S) {
   extern __shared__ __align__(128) double sm[];
-  double* const vbuf0 = sm + 2 * kTileMax;  // kVecMax + 2: task vectors (double-buffered)
-  double* const vbuf1 = vbuf0 + kVecMax + 2;
-  double* const vec2 = vbuf1 + kVecMax + 2;   // kVecMax: accumulators
-  double* const red = vec2 + kVecMax;         // kSweepThreads
-  __shared__ __align__(8) uint64_t mbar[2];
+  // kStages tile slots (a ring: kStages - 1 tiles stream while one is computed on),
+  // kVecSlots task-vector slots, accumulators, reduction scratch
+  double* const vbase = sm + kStages * kTileMax;  // kVecSlots x (kVecMax + 2)
+  double* const vec2 = vbase + kVecSlots * (kVecMax + 2);  // kVecMax: accumulators
+  double* const red = vec2 + kVecMax;                       // kSweepThreads
+  __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
@@ -166,13 +167,11 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   const unsigned long long grid = gridDim.x;
   if (tid == 0) {
     atomicMin(&S.ctl[SW_T0], globaltimer());
-    mbar_init(&mbar[0]);
-    mbar_init(&mbar[1]);
+    for (int q = 0; q < kStages; ++q) mbar_init(&mbar[q]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t par0 = 0u, par1 = 0u;
-  int buf = 0;
+  uint32_t parbits = 0u;  // phase parity of every ring slot
   const size_t gthreads = (size_t)gridDim.x * kSweepThreads;
   const size_t gtid = (size_t)blockIdx.x * kSweepThreads + tid;
 
@@ -212,7 +211,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         const int k = (i & 1) ? i * G + (G - 1 - b) : i * G + b;
         return k < ntk ? k : -1;
       };
-      // thread 0: stream tdesc[kk] into stage `bf`, plus (vbytes > 0) a task vector
+      // thread 0: stream tdesc[kk] into ring slot `bf`, plus (vbytes > 0) the task
+      // vector into vector slot `vs`
       auto prefetch = [&](int kk, int bf, long long vlo2, int vbytes, int vs) {
         const int4 d = S.tdesc[kk];
         const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
@@ -227,34 +227,47 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         if (vbytes > 0)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(vs ? vbuf1 : vbuf0)),
+                  smem_u32(vbase + vs * (kVecMax + 2))),
               "l"(S.vb + vlo2), "r"((uint32_t)vbytes), "r"(smem_u32(&mbar[bf]))
               : "memory");
       };
+      // thread 0's prefetch cursor over this CTA's tile stream (task pi, tile pk)
+      int pi = 0, pk = 0, pk1 = 0, ps = 0;
+      long long pvlo = 0;
+      int pvb = 0;
+      auto cursor_load = [&]() {
+        const int kt = task_of(pi);
+        if (kt >= 0) { pk = MT[kt].k0; pk1 = MT[kt].k1; pvlo = MT[kt].vlo2; pvb = MT[kt].vbytes; }
+        else pk = pk1 = 0;
+      };
+      auto issue_next = [&]() {  // thread 0
+        if (pk >= pk1) return;
+        const bool first = pk == MT[task_of(pi)].k0;
+        prefetch(pk, ps % kStages, pvlo, first ? pvb : 0, pi % kVecSlots);
+        ++ps;
+        if (++pk >= pk1) { ++pi; cursor_load(); }
+      };
       if (tid == 0) {
-        const int k0 = task_of(0);
-        if (k0 >= 0) prefetch(MT[k0].k0, buf, MT[k0].vlo2, MT[k0].vbytes, 0);
+        cursor_load();
+        for (int q = 0; q < kStages; ++q) issue_next();
       }
+      int cs = 0;  // tiles consumed in this phase
       for (int i = 0;; ++i) {
         const int k = task_of(i);
         if (k < 0) break;
         const MTaskDesc D = MT[k];
-        const int vs = i & 1;
-        // thread 0: what to stream after this task's last tile
-        int nk0 = -1, nvb = 0;
-        long long nvlo = 0;
-        if (tid == 0) {
-          const int kn = task_of(i + 1);
-          if (kn >= 0) { nk0 = MT[kn].k0; nvlo = MT[kn].vlo2; nvb = MT[kn].vbytes; }
-        }
-        const double* const vv = (vs ? vbuf1 : vbuf0) + D.voff;  // this task's vector
-        auto next_tile_and_wait = [&](int kk) {
-          if (tid == 0) {
-            if (kk + 1 < D.k1) prefetch(kk + 1, buf ^ 1, 0, 0, 0);
-            else if (nk0 >= 0) prefetch(nk0, buf ^ 1, nvlo, nvb, vs ^ 1);
-          }
-          if (buf) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
-          else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
+        const double* const vv = vbase + (i % kVecSlots) * (kVecMax + 2) + D.voff;  // this task's vector
+        int buf = 0;
+        // wait for the next tile of the stream (its ring slot becomes `buf`)
+        auto next_tile_and_wait = [&](int) {
+          buf = cs % kStages;
+          mbar_wait(&mbar[buf], (parbits >> buf) & 1u);
+          parbits ^= 1u << buf;
+        };
+        // after the tile's last read (callers __syncthreads first): refill its slot
+        auto tile_done = [&]() {
+          if (tid == 0) issue_next();
+          ++cs;
         };
         if (D.big == 2) {
           // ---------------- strip of a wide supernode (nr <= kVecMax): fwd = rows
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             tile_matvec_t(T, D.nr, D.cols, vv, [&](int j, double y) { xb[j] = y; });
           }
           __syncthreads();
-          buf ^= 1;
+          tile_done();
         } else if (!D.big) {
           // ---------------- small supernode: all column tiles, one CTA
           for (int kk = D.k0; kk < D.k1; ++kk) {
@@ -292,7 +305,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
               tile_matvec_t(T, D.nr, cols, vv, [&](int j, double y) { xb[j] = y; });
             }
             __syncthreads();
-            buf ^= 1;
+            tile_done();
           }
           if (fwd) {
             double* const upd = S.upd + D.uptr;
@@ -319,7 +332,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
               else tile_matvec_t(T, rows, D.cols, vv + j * D.RB, [&](int c, double y) { vec2[c] += y; });
             }
             __syncthreads();
-            buf ^= 1;
+            tile_done();
           }
           {
             double* const part = (fwd ? S.fpart : S.bpart) + D.part;
