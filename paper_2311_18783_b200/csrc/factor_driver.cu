@@ -81,6 +81,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
     mode[g] = nr <= dev::kVecMax ? ((int64_t)nr * nc <= dev::kSingleMax ? 0 : 1) : 2;
+    if (mode[g] == 1 && getenv("MDD_FORCE_2D")) mode[g] = 2;  // debug: no strips
     if (mode[g] == 0) {
       const int CB = std::max(1, std::min(nc, dev::kTileMax / nr));
       vRB[g] = nr; vCB[g] = CB;
@@ -92,8 +93,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       for (int r0 = 0; r0 < nr; r0 += rs) ft[g].push_back(add_tile(make_int4(g, r0, 0, 1), std::min(rs, nr - r0), nc));
       for (int c0 = 0; c0 < nc; c0 += cs) bt[g].push_back(add_tile(make_int4(g, 0, c0, 2), nr, std::min(cs, nc - c0)));
     } else {
+      // a task's vector (up to kGroup row blocks / column blocks) must fit a
+      // kVecMax shared-memory slot: RB, CB <= kVecMax / kGroup
       const int CB = std::min(nc, 64);
-      const int RB = std::max(1, dev::kTileMax / CB);
+      const int RB = std::max(1, std::min(dev::kVecMax / 4, dev::kTileMax / CB));
       const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;   // sized for groups of one tile
@@ -176,6 +179,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
     MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
     sweep_grid = nsm * per_sm;
+    if (const char* ev = getenv("MDD_SWEEP_GRID")) {  // debug: fewer persistent CTAs
+      const int gr = atoi(ev);
+      if (gr > 0 && gr < sweep_grid) sweep_grid = gr;
+    }
   }
   for (int dir = 0; dir < 2; ++dir) {
     std::vector<dev::MTaskDesc>& out = dir == 0 ? mtf : mtb;
@@ -270,6 +277,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
           }
         }
       }
+      for (const Cand& c : lt)
+        MDD_REQUIRE(c.d.vbytes <= (int)((dev::kVecMax + 2) * sizeof(double)), 5,
+                    "sweep task vector exceeds its shared-memory slot");
       std::stable_sort(lt.begin(), lt.end(), [](const Cand& x, const Cand& y) { return x.bytes > y.bytes; });
       for (auto& c : lt) {
         dev::MTaskDesc X = c.d;

@@ -374,6 +374,9 @@ __global__ void __launch_bounds__(kSweepThreads, 2) k_sweep(SweepDev S) {
         __syncthreads();
       }
     }
+    // the next phases read vb / upd / xf / xb with TMA bulk copies (async proxy):
+    // order this thread's generic-proxy global writes before them
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     if (S.trace && tid == 0) {
       S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x)] = t_ph;
       S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x) + 1] = globaltimer();

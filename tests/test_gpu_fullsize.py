@@ -94,3 +94,29 @@ def test_pcg_full_size(c1):
     assert np.linalg.norm(f - A @ xh) <= 1e-3 * np.linalg.norm(f)
     it2, rel2, ok2 = G.solve(dev(f), x, tol=1e-8)
     assert it2 == it and np.array_equal(x.cpu().numpy(), xh)   # bit-reproducible
+
+
+def test_sweep_is_grid_independent_and_reproducible():
+    # the persistent sweep's partial sums are combined in a fixed order, so the
+    # result must not depend on how many CTAs run it (a race or a shared-memory
+    # overrun shows up here first); MDD_SWEEP_GRID caps the persistent grid
+    import os
+    from paper_2311_18783_b200 import MaxwellDD
+    w = workloads.make("c1", n=16, p=4)
+    outs = {}
+    for grid in ("0", "5"):
+        os.environ["MDD_SWEEP_GRID"] = grid
+        try:
+            G = MaxwellDD(w)
+        finally:
+            os.environ.pop("MDD_SWEEP_GRID", None)
+        g = torch.Generator(device="cuda").manual_seed(0)
+        v = torch.randn(G.n, dtype=torch.float64, device="cuda", generator=g)
+        y = [torch.empty_like(v) for _ in range(3)]
+        G.apply_local(v, y[0])
+        G.apply_coarse(v, y[1])
+        G.apply_preconditioner(v, y[2])
+        outs[grid] = [t.cpu().numpy() for t in y]
+        G.close()
+    for a, b in zip(outs["0"], outs["5"]):
+        assert np.array_equal(a, b)
