@@ -93,11 +93,11 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
 enum { SW_EPOCH = 0, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR };
 constexpr int kSweepThreads = 256;
-constexpr int kTileMax = 2176;   // doubles per tile (17 KB, one TMA bulk copy)
+constexpr int kTileMax = 3328;   // doubles per tile (26 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
-constexpr int kStages = 3;       // tile ring slots per CTA (two tiles stream while one computes)
-constexpr int kVecSlots = 4;     // task-vector slots (> the tasks the ring can span)
+constexpr int kStages = 2;       // tile ring slots per CTA (one tile streams while one computes)
+constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can span)
 constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
 
 // one task of an M phase (factor_driver.cu builds them, forward and backward)

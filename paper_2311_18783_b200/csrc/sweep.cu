@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   double* const vec2 = vbase + kVecSlots * (kVecMax + 2);  // kVecMax: accumulators
   double* const red = vec2 + kVecMax;                       // kSweepThreads
   __shared__ __align__(8) uint64_t mbar[kStages];
-  __shared__ __align__(16) MTaskDesc s_desc[8];
+  __shared__ __align__(16) MTaskDesc s_desc[4];
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
@@ -232,33 +232,35 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
               "l"(S.vb + vlo2), "r"((uint32_t)vbytes), "r"(smem_u32(&mbar[bf]))
               : "memory");
       };
-      // this CTA's task descriptors stream into an 8-slot shared-memory ring with
-      // cp.async, four tasks ahead (no descriptor load on any critical path)
+      // this CTA's task descriptors stream into a 4-slot shared-memory ring with
+      // cp.async, three tasks ahead (no descriptor load on any critical path)
       constexpr int kDW = (int)(sizeof(MTaskDesc) / 16);  // 16-byte words per descriptor
       auto desc_fetch = [&](int i) {  // threads < kDW: one commit group per call
         if (tid < kDW) {
           const int kt = task_of(i);
           if (kt >= 0)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(
-                             reinterpret_cast<const int4*>(&s_desc[i & 7]) + tid)),
+                             reinterpret_cast<const int4*>(&s_desc[i & 3]) + tid)),
                          "l"(reinterpret_cast<const int4*>(MT + kt) + tid)
                          : "memory");
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
       };
-      for (int q = 0; q < 4; ++q) desc_fetch(q);
+      desc_fetch(0);
+      desc_fetch(1);
+      desc_fetch(2);
       if (tid < kDW) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
       // thread 0's prefetch cursor over this CTA's tile stream (task pi, tile pk);
-      // it runs at most kStages tiles ahead, i.e. <= 3 tasks past the current one
+      // it runs at most kStages tiles ahead, i.e. <= 2 tasks past the current one
       int pi = 0, pk = 0, pk1 = 0, ps = 0;
       auto cursor_load = [&]() {
-        if (task_of(pi) >= 0) { pk = s_desc[pi & 7].k0; pk1 = s_desc[pi & 7].k1; }
+        if (task_of(pi) >= 0) { pk = s_desc[pi & 3].k0; pk1 = s_desc[pi & 3].k1; }
         else pk = pk1 = 0;
       };
       auto issue_next = [&]() {  // thread 0
         if (pk >= pk1) return;
-        const MTaskDesc& Dp = s_desc[pi & 7];
+        const MTaskDesc& Dp = s_desc[pi & 3];
         const bool first = pk == Dp.k0;
         prefetch(pk, ps % kStages, Dp.vlo2, first ? Dp.vbytes : 0, pi % kVecSlots);
         ++ps;
@@ -274,10 +276,10 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         if (k < 0) break;
         // descriptors i+1, i+2 must be resident before the cursor reaches them;
         // task i+3's starts streaming now
-        desc_fetch(i + 4);
+        desc_fetch(i + 3);
         if (tid < kDW) asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        const MTaskDesc D = s_desc[i & 7];
+        const MTaskDesc D = s_desc[i & 3];
         const double* const vv = vbase + (i % kVecSlots) * (kVecMax + 2) + D.voff;  // this task's vector
         int buf = 0;
         // wait for the next tile of the stream (its ring slot becomes `buf`)
