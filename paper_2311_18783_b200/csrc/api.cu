@@ -36,6 +36,11 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+int env_int(const char* k, int d) {
+  const char* v = getenv(k);
+  return v ? atoi(v) : d;
+}
+
 // static-pivot threshold of the coarse LDL^T (unit-diagonal scaled E)
 const double kCoarsePivotTol = 1e-14;
 
@@ -478,7 +483,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     }
     std::vector<SymSystem> sys(nsub);
     for (int i = 0; i < nsub; ++i) sys[i] = SymSystem{&lpat[i], lxyz[i].data(), lslot[i].data()};
-    build_factor_plan(H->loc.fp, sys, 64);
+    build_factor_plan(H->loc.fp, sys, env_int("MDD_ND_LEAF", 64));
     H->loc.name = "local";
     // position -> global dof, global dof -> positions (subdomain order)
     const FactorPlan& fp = H->loc.fp;
@@ -766,7 +771,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     SymSystem esys{&epat, exyz.data(), eslot.data()};
     esys.last = elast.data();
     std::vector<SymSystem> sys{esys};
-    build_factor_plan(H->crs.fp, sys, 64);
+    build_factor_plan(H->crs.fp, sys, env_int("MDD_ND_LEAF", 64));
     H->crs.name = "coarse";
     H->crs.upload();
     H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);

@@ -83,9 +83,16 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     mode[g] = nr <= dev::kVecMax ? ((int64_t)nr * nc <= dev::kSingleMax ? 0 : 1) : 2;
     if (mode[g] == 1 && getenv("MDD_FORCE_2D")) mode[g] = 2;  // debug: no strips
     if (mode[g] == 0) {
-      const int CB = std::max(1, std::min(nc, dev::kTileMax / nr));
-      vRB[g] = nr; vCB[g] = CB;
-      for (int c0 = 0; c0 < nc; c0 += CB) ft[g].push_back(add_tile(make_int4(g, 0, c0, 3), nr, std::min(CB, nc - c0)));
+      // packed column tiles (no zeros above the diagonal), as many columns as fit
+      vRB[g] = nr; vCB[g] = nc;
+      for (int c0 = 0; c0 < nc;) {
+        int cols = 0;
+        int64_t sz = 0;
+        while (c0 + cols < nc && sz + (nr - c0 - cols) <= dev::kTileMax) { sz += nr - c0 - cols; ++cols; }
+        MDD_REQUIRE(cols > 0, 5, "small supernode column does not fit a tile");
+        ft[g].push_back(add_tile(make_int4(g, cols, c0, 3), (int)sz, 1));
+        c0 += cols;
+      }
       bt[g] = ft[g];
     } else if (mode[g] == 1) {
       const int rs = std::max(1, dev::kTileMax / nc), cs = std::max(1, dev::kTileMax / nr);
@@ -157,7 +164,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   std::vector<int4> td;
   std::vector<int> lev_f(fp.nlevels + 1, 0), lev_b(fp.nlevels + 1, 0);
   auto push_td = [&](int t) {
-    td.push_back(make_int4(t, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
+    // .x: tile id, or for packed small tiles first column | columns << 16 (the kernel
+    // needs them per tile)
+    const int x = tl[t].w == 3 ? (tl[t].z | (tl[t].y << 16)) : t;
+    td.push_back(make_int4(x, tile_bytes(t), (int)(uint32_t)(toff[t] & 0xffffffffu), (int)(uint32_t)(toff[t] >> 32)));
   };
   auto set_vec = [](dev::MTaskDesc& X, int64_t lo, int64_t hi) {
     X.vlo2 = lo & ~1LL;

@@ -150,6 +150,75 @@ __device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, con
     if (lane == 0) fin(j, s);
   }
 }
+// Packed lower-trapezoidal column tile of a small supernode: columns c0 .. c0+C-1
+// of an nr-row panel, column jj holding rows c0+jj .. nr-1 (the zeros above the
+// diagonal are not stored), column offsets coff(jj) = jj (nr - c0) - jj (jj - 1) / 2.
+// Forward: y_i = sum_{jj <= i - c0} T(i, c0 + jj) v[jj] for rows i in [c0, nr);
+// fin(i, y) once per row.
+template <class Fin>
+__device__ __forceinline__ void tile_matvec_packed(const double* T, int nr, int c0, int C, const double* v,
+                                                   double* red, Fin fin) {
+  const int tid = threadIdx.x;
+  const int R = nr - c0;  // rows this tile touches
+  if (R > kSweepThreads / 2) {
+    for (int ip = tid; ip < R; ip += kSweepThreads) {
+      const int jb = min(C, ip + 1);
+      double s0 = 0.0, s1 = 0.0;
+      int addr = ip, jj = 0;
+      for (; jj + 2 <= jb; jj += 2) {
+        s0 += T[addr] * v[jj];
+        addr += R - jj - 1;
+        s1 += T[addr] * v[jj + 1];
+        addr += R - jj - 2;
+      }
+      if (jj < jb) s0 += T[addr] * v[jj];
+      fin(c0 + ip, s0 + s1);
+    }
+    return;
+  }
+  const int Rp = R >= 32 ? (R + 31) & ~31 : (R > 16 ? 32 : R > 8 ? 16 : R > 4 ? 8 : R > 2 ? 4 : R);
+  const int nsl = max(1, min(kSweepThreads / Rp, C));
+  const int ip = tid % Rp, sl = tid / Rp;
+  if (sl < nsl && ip < R) {
+    const int ja = (sl * C) / nsl, jb = min(((sl + 1) * C) / nsl, ip + 1);
+    double s0 = 0.0;
+    // address of (row c0+ip, column jj): coff(jj) + ip - jj
+    int addr = ja * R - (ja * (ja - 1)) / 2 + ip - ja;
+    for (int jj = ja; jj < jb; ++jj) {
+      s0 += T[addr] * v[jj];
+      addr += R - jj - 1;
+    }
+    red[sl * Rp + ip] = s0;
+  }
+  __syncthreads();
+  for (int q2 = tid; q2 < R; q2 += kSweepThreads) {
+    double s = 0.0;
+    for (int q = 0; q < nsl; ++q) s += red[q * Rp + q2];
+    fin(c0 + q2, s);
+  }
+}
+
+// Backward on a packed tile: x_jj = sum_{i >= c0+jj} T(i, c0+jj) w[i]; fin(jj, x)
+template <class Fin>
+__device__ __forceinline__ void tile_matvec_t_packed(const double* T, int nr, int c0, int C, const double* w,
+                                                     Fin fin) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = nr - c0;
+  for (int jj = warp; jj < C; jj += kWarps) {
+    const double* col = T + (jj * R - (jj * (jj - 1)) / 2);
+    const double* wj = w + c0 + jj;
+    const int len = R - jj;
+    double s0 = 0.0, s1 = 0.0;
+    int i = lane;
+    for (; i + 32 < len; i += 64) {
+      s0 += col[i] * wj[i];
+      s1 += col[i + 32] * wj[i + 32];
+    }
+    if (i < len) s0 += col[i] * wj[i];
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) fin(jj, s);
+  }
+}
 }  // namespace
 
 __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
@@ -161,6 +230,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   double* const red = vec2 + kVecMax;                       // kSweepThreads
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ __align__(16) MTaskDesc s_desc[4];
+  __shared__ int s_tinfo[kStages];
   __shared__ int s_flag;
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
@@ -216,6 +286,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       // vector into vector slot `vs`
       auto prefetch = [&](int kk, int bf, long long vlo2, int vbytes, int vs) {
         const int4 d = S.tdesc[kk];
+        s_tinfo[bf] = d.x;  // read by the consumer after at least one __syncthreads
         const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[bf])),
                      "r"((uint32_t)d.y + (uint32_t)vbytes)
@@ -314,19 +385,20 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           tile_done();
         } else if (!D.big) {
           // ---------------- small supernode: all column tiles, one CTA
+          // packed column tiles: tdesc.x = first column | columns << 16
           for (int kk = D.k0; kk < D.k1; ++kk) {
-            const int cb = kk - D.k0;
-            const int cols = min(D.CB, D.nc - cb * D.CB);
             next_tile_and_wait(kk);
+            const int cx = s_tinfo[buf];  // written by thread 0 with the tile's bulk copy
+            const int c0 = cx & 0xffff, cols = cx >> 16;
             const double* T = sm + buf * kTileMax;
             if (fwd) {
-              if (cb == 0)
-                tile_matvec(T, D.nr, cols, vv, red, [&](int r, double y) { vec2[r] = y; });
+              if (c0 == 0)
+                tile_matvec_packed(T, D.nr, 0, cols, vv, red, [&](int r, double y) { vec2[r] = y; });
               else
-                tile_matvec(T, D.nr, cols, vv + cb * D.CB, red, [&](int r, double y) { vec2[r] += y; });
+                tile_matvec_packed(T, D.nr, c0, cols, vv + c0, red, [&](int r, double y) { vec2[r] += y; });
             } else {
-              double* const xb = S.xb + D.col0 + cb * D.CB;
-              tile_matvec_t(T, D.nr, cols, vv, [&](int j, double y) { xb[j] = y; });
+              double* const xb = S.xb + D.col0 + c0;
+              tile_matvec_t_packed(T, D.nr, c0, cols, vv, [&](int j, double y) { xb[j] = y; });
             }
             __syncthreads();
             tile_done();
@@ -420,7 +492,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
 
 // relayout of the column-major panels into contiguous tiles (setup).  tiles[k] =
 // {g, a, b, kind}: 0 2-D (rb, cb), 1 forward row strip (first row a, all columns),
-// 2 backward column strip (all rows, first column b), 3 small column tile (b)
+// 2 backward column strip (all rows, first column b), 3 small packed column tile
+// (a = columns, b = first column)
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,
                                 const int64_t* __restrict__ lptr) {
   const int k = blockIdx.x;
@@ -438,8 +511,23 @@ __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict
   } else {
     c0 = tl.z; cols = min(CB, nc - c0);
   }
-  const double* src = L + lptr[g] + (i64)c0 * nr + r0;
   double* dst = const_cast<double*>(S.Lt) + S.tile_off[k];
+  if (kind == 3) {
+    // packed: column jj of the tile (panel column c0 + jj) keeps rows c0 + jj .. nr-1
+    c0 = tl.z;
+    cols = tl.y;
+    const int R = nr - c0;
+    int off = 0;
+    for (int jj = 0; jj < cols; ++jj) {
+      const int len = R - jj;
+      const double* src = L + lptr[g] + (i64)(c0 + jj) * nr + (c0 + jj);
+      for (int q = threadIdx.x; q < len; q += blockDim.x) dst[off + q] = src[q];
+      off += len;
+    }
+    if (threadIdx.x == 0 && (off & 1)) dst[off] = 0.0;
+    return;
+  }
+  const double* src = L + lptr[g] + (i64)c0 * nr + r0;
   for (int q = threadIdx.x; q < rows * cols; q += blockDim.x) {
     const int j = q / rows, i = q % rows;
     dst[q] = src[(i64)j * nr + i];

@@ -8,6 +8,8 @@
 // applied by hand-written level-scheduled triangular-solve kernels".
 #include "common.h"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <numeric>
 
@@ -246,7 +248,11 @@ void analyse_one(Sys1& s, const SymSystem& sys, int leaf) {
     i64 merged = (nc * (nc + 1)) / 2 + nc * nop;
     i64 orig = (nck * (nck + 1)) / 2 + nck * nok + (ncp * (ncp + 1)) / 2 + ncp * nop;
     i64 z = merged - orig;
-    bool ok = (nc <= 8) || (nc <= 32 && z * 5 <= merged) || (z * 20 <= merged);
+    // relaxed amalgamation (MDD_AMALG=1: more aggressive, fewer levels and supernodes
+    // for the latency-bound sweep at the cost of explicit zeros)
+    static const int aggressive = getenv("MDD_AMALG") ? atoi(getenv("MDD_AMALG")) : 0;
+    bool ok = aggressive ? ((nc <= 16) || (nc <= 64 && z * 3 <= merged) || (z * 8 <= merged))
+                         : ((nc <= 8) || (nc <= 32 && z * 5 <= merged) || (z * 20 <= merged));
     if (!ok) continue;
     first[p] = first[k];
     alive[k] = 0;
