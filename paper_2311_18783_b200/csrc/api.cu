@@ -886,6 +886,9 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         H->nbzt = (int)bzt.size();
         H->nbz = (int)bz.size();
         H->u_loc.alloc(lp.ntot);
+        // positions of subdomains without GenEO vectors are never written by
+        // k_geneo_z but are read by k_z_apply's prolongation: they must stay 0
+        H->u_loc.zero(s);
         CUDA_CHECK(cudaStreamSynchronize(s));
       }
       // the mixed CSR copies are not needed on the hot path
