@@ -78,9 +78,12 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     off += ((int64_t)rows * cols + 1) & ~1LL;  // 16-byte aligned tiles
     return (int)tl.size() - 1;
   };
+  const int64_t single_max = getenv("MDD_SINGLE_MAX") ? atoll(getenv("MDD_SINGLE_MAX")) : dev::kSingleMax;
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
-    mode[g] = nr <= dev::kVecMax ? ((int64_t)nr * nc <= dev::kSingleMax ? 0 : 1) : 2;
+    // a supernode one CTA sweeps alone must stay short (it is a phase's critical path
+    // on the upper, latency-bound levels): at most ~kSingleMax stored entries
+    mode[g] = nr <= dev::kVecMax ? ((int64_t)nr * nc <= single_max ? 0 : 1) : 2;
     if (mode[g] == 1 && getenv("MDD_FORCE_2D")) mode[g] = 2;  // debug: no strips
     if (mode[g] == 0) {
       // packed column tiles (no zeros above the diagonal), as many columns as fit
