@@ -153,6 +153,21 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ B200 arm
+def reduce_over_ranks(ms, work, world, device):
+    """Whole-job aggregation: the slowest rank's time (max) and every rank's work
+    (sum).  Ranks solve independent replicas (no data-path collective); this is
+    the only collective of the bench."""
+    if world <= 1:
+        return float(ms), float(work)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    w = torch.tensor([float(work)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    return float(t[0]), float(w[0])
+
+
 def main():
     args = parse()
     rank = _env_int("RANK", 0)
@@ -224,17 +239,7 @@ def main():
         dist.barrier()
     clocks = clk.stop()
     step_ms = t_ms / args.steps
-    # max over ranks
-    tt = torch.tensor([step_ms, float(work)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tmax = tt.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        step_ms_max = float(tmax[0])
-        total_work = float(tt[1])
-    else:
-        step_ms_max = step_ms
-        total_work = float(work)
+    step_ms_max, total_work = reduce_over_ranks(step_ms, work, world, "cuda")
     value = total_work / (step_ms_max * args.steps / 1e3)
     in_step = ((sw1[0] - sw0[0]) / max(1, sw1[1] - sw0[1]), sw1[1] - sw0[1])
 
@@ -271,13 +276,8 @@ def main():
         _, it, _ = G.solve_host_into(fp.numpy(), xp.numpy(), tol=TOL, maxit=args.maxit)
         e2e_ms += (time.perf_counter() - t0) * 1e3
         e2e_work += n * it
-    e2e_val = e2e_work / (e2e_ms / 1e3)
-    if world > 1:
-        ev = torch.tensor([e2e_ms, float(e2e_work)], dtype=torch.float64, device="cuda")
-        em = ev.clone()
-        dist.all_reduce(em, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
-        e2e_val = float(ev[1]) / (float(em[0]) / 1e3)
+    e2e_ms_max, e2e_total = reduce_over_ranks(e2e_ms, e2e_work, world, "cuda")
+    e2e_val = e2e_total / (e2e_ms_max / 1e3)
 
     info = G.info
     roof = roofline(G, sweep_ms, in_step)
