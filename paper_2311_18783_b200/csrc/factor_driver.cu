@@ -4,6 +4,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
 #include "device.h"
 
 namespace mdd {
@@ -464,6 +467,23 @@ void DevFactor::check_abort(cudaStream_t s) {
   }
 }
 
+namespace {
+#define CUBLAS_OK(x)                                                                                \
+  do {                                                                                              \
+    cublasStatus_t s__ = (x);                                                                       \
+    if (s__ != CUBLAS_STATUS_SUCCESS)                                                               \
+      throw Error(1, std::string(#x) + ": cublas status " + std::to_string((int)s__));              \
+  } while (0)
+#define CUSOLVER_OK(x)                                                                              \
+  do {                                                                                              \
+    cusolverStatus_t s__ = (x);                                                                     \
+    if (s__ != CUSOLVER_STATUS_SUCCESS)                                                             \
+      throw Error(1, std::string(#x) + ": cusolver status " + std::to_string((int)s__));            \
+  } while (0)
+constexpr int kBigFront = 1024;  // fronts with more rows take the blocked path
+constexpr int kPanel = 64;
+}  // namespace
+
 int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s) {
   DBuf<double> fronts, umat;
   fronts.alloc(std::max<int64_t>(fp.fsize, 1));
@@ -473,13 +493,95 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
   err.zero(s);
   L.zero(s);
   dev::PlanDev P = plan();
+  // per level: small fronts in one launch (one CTA each), big fronts blocked with
+  // cuBLAS trailing updates, cuSOLVER triangular inverse and cuBLAS M21 = L21 L11^{-1}
+  std::vector<int> small_list;
+  std::vector<int> small_ptr(fp.nlevels + 1, 0);
+  std::vector<std::vector<int>> big(fp.nlevels);
+  int64_t wmax = 1;
   for (int l = 0; l < fp.nlevels; ++l) {
-    int cnt = fp.level_ptr[l + 1] - fp.level_ptr[l];
-    dev::k_mf_factor_level<<<cnt, 256, 0, s>>>(P, fp.level_ptr[l], src, fronts.p, L.p, dinv.p,
-                                               umat.p, mode, tol, dropped, err.p);
-    CUDA_CHECK(cudaGetLastError());
+    small_ptr[l] = (int)small_list.size();
+    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+      const int g = fp.level_sn[k];
+      const int nr = fp.sn_ncol[g] + fp.sn_noff[g];
+      if (nr > kBigFront) {
+        big[l].push_back(g);
+        wmax = std::max<int64_t>(wmax, (int64_t)nr * kPanel);
+      } else {
+        small_list.push_back(g);
+      }
+    }
   }
-  CUDA_CHECK(cudaStreamSynchronize(s));
+  small_ptr[fp.nlevels] = (int)small_list.size();
+  DBuf<int> dsmall;
+  dsmall.upload(small_list.empty() ? std::vector<int>{0} : small_list);
+  bool any_big = false;
+  for (auto& b : big) any_big |= !b.empty();
+  cublasHandle_t cb = nullptr;
+  cusolverDnHandle_t cs = nullptr;
+  DBuf<double> W;
+  DBuf<char> trw;
+  DBuf<int> info;
+  if (any_big) {
+    CUBLAS_OK(cublasCreate(&cb));
+    CUBLAS_OK(cublasSetStream(cb, s));
+    CUSOLVER_OK(cusolverDnCreate(&cs));
+    CUSOLVER_OK(cusolverDnSetStream(cs, s));
+    W.alloc(wmax);
+    info.alloc(1);
+  }
+  try {
+    for (int l = 0; l < fp.nlevels; ++l) {
+      const int cnt = small_ptr[l + 1] - small_ptr[l];
+      if (cnt > 0) {
+        dev::k_mf_factor_level<<<cnt, 256, 0, s>>>(P, dsmall.p + small_ptr[l], src, fronts.p, L.p, dinv.p,
+                                                   umat.p, mode, tol, dropped, err.p);
+        CUDA_CHECK(cudaGetLastError());
+      }
+      for (int g : big[l]) {
+        const int nc = fp.sn_ncol[g], no = fp.sn_noff[g], nr = nc + no;
+        double* F = fronts.p + fp.sn_fptr[g];
+        double* Lp = L.p + fp.sn_lptr[g];
+        dev::k_front_assemble<<<256, 256, 0, s>>>(P, g, src, fronts.p, umat.p);
+        dev::k_front_assemble2<<<1, 1024, 0, s>>>(P, g, src, fronts.p, umat.p);
+        for (int j0 = 0; j0 < nc; j0 += kPanel) {
+          const int nb = std::min(kPanel, nc - j0);
+          dev::k_panel_factor<<<1, 512, 0, s>>>(P, g, j0, nb, fronts.p, dinv.p, W.p, mode, tol, dropped, err.p);
+          const int rest = nr - (j0 + nb);
+          if (rest > 0) {
+            const double m1 = -1.0, one = 1.0;
+            // F22 -= W L_p^T (lower triangle), W = L_p D_p
+            CUBLAS_OK(cublasDsyrkx(cb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, rest, nb, &m1, W.p, rest,
+                                   F + (int64_t)j0 * nr + (j0 + nb), nr, &one,
+                                   F + (int64_t)(j0 + nb) * nr + (j0 + nb), nr));
+          }
+        }
+        dev::k_front_finish_copy<<<256, 256, 0, s>>>(P, g, fronts.p, L.p, umat.p);
+        // L11^{-1} in place (unit lower), then M21 = L21 L11^{-1}
+        size_t dws = 0, hws = 0;
+        CUSOLVER_OK(cusolverDnXtrtri_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_UNIT, nc, CUDA_R_64F, Lp,
+                                                nr, &dws, &hws));
+        if (trw.n < dws + 8) trw.alloc(dws + 8);
+        std::vector<char> hbuf(std::max<size_t>(hws, 1));
+        CUSOLVER_OK(cusolverDnXtrtri(cs, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_UNIT, nc, CUDA_R_64F, Lp, nr, trw.p,
+                                     dws, hbuf.data(), hws, info.p));
+        if (no > 0) {
+          const double one = 1.0;
+          CUBLAS_OK(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_UNIT, no, nc,
+                                &one, Lp, nr, F + nc, nr, Lp + nc, nr));
+        }
+        dev::k_front_fold_d<<<256, 256, 0, s>>>(P, g, L.p, dinv.p);
+        CUDA_CHECK(cudaGetLastError());
+      }
+    }
+    CUDA_CHECK(cudaStreamSynchronize(s));
+  } catch (...) {
+    if (cb) cublasDestroy(cb);
+    if (cs) cusolverDnDestroy(cs);
+    throw;
+  }
+  if (cb) cublasDestroy(cb);
+  if (cs) cusolverDnDestroy(cs);
   int e = 0;
   CUDA_CHECK(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (mode != 2) MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");

@@ -162,11 +162,11 @@ __global__ void k_scale_csr(int n, const int* __restrict__ ptr, const int* __res
 }
 
 // --------------------------------------------------- multifrontal LDL^T
-__global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
+__global__ void k_mf_factor_level(PlanDev P, const int* __restrict__ list, const double* __restrict__ src,
                                   double* __restrict__ fronts, double* __restrict__ L,
                                   double* __restrict__ dinv, double* __restrict__ umat, int mode,
                                   double tol, uint8_t* __restrict__ dropped, int* __restrict__ err) {
-  const int g = P.level_sn[level_begin + blockIdx.x];
+  const int g = list[blockIdx.x];
   const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
   const i64 col0 = P.sn_col0[g];
   double* F = fronts + P.sn_fptr[g];
@@ -264,6 +264,128 @@ __global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __re
   // fold D^{-1} into the rows of the diagonal block: the forward sweep then yields
   // z_c = D^{-1} L11^{-1} t_c directly; the backward sweep divides z_c by D^{-1}
   // again in its gather (sweep.cu, G_b)
+  for (i64 k = tid; k < (i64)nc * nc; k += nt) {
+    const int j = (int)(k / nc), i = (int)(k % nc);
+    if (i >= j) Lp[(i64)j * nr + i] *= dinv[col0 + i];
+  }
+}
+
+
+// ---------------------------------------------- big fronts (blocked, cuBLAS updates)
+// assemble one front: zero, original entries, children's update matrices
+__global__ void k_front_assemble(PlanDev P, int g, const double* __restrict__ src, double* __restrict__ fronts,
+                                 const double* __restrict__ umat) {
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  double* F = fronts + P.sn_fptr[g];
+  const int tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
+  for (i64 k = tid; k < (i64)nr * nr; k += nt) F[k] = 0.0;
+}
+__global__ void k_front_assemble2(PlanDev P, int g, const double* __restrict__ src, double* __restrict__ fronts,
+                                  const double* __restrict__ umat) {
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  double* F = fronts + P.sn_fptr[g];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (i64 a = P.asm_ptr[g] + tid; a < P.asm_ptr[g + 1]; a += nt) F[P.asm_pos[a]] += src[P.asm_src[a]];
+  __syncthreads();
+  for (i64 ci = P.child_ptr[g]; ci < P.child_ptr[g + 1]; ++ci) {
+    const int c = P.child_list[ci];
+    const int noc = P.sn_noff[c];
+    const double* U = umat + P.sn_umptr[c];
+    const int* rm = P.relmap + P.sn_rowptr[c];
+    for (i64 k = tid; k < (i64)noc * noc; k += nt) {
+      int b = (int)(k / noc), a = (int)(k % noc);
+      if (a >= b) F[(i64)rm[b] * nr + rm[a]] += U[k];
+    }
+    __syncthreads();
+  }
+}
+
+// factor panel columns [j0, j0+nb) of a front (right-looking inside the panel, same
+// pivot rules as k_mf_factor_level), then W = L_panel D_panel for the rows below
+// the panel (n_rest x nb, ld n_rest) for the trailing update F22 -= W L_panel^T
+__global__ void k_panel_factor(PlanDev P, int g, int j0, int nb, double* __restrict__ fronts,
+                               double* __restrict__ dinv, double* __restrict__ W, int mode, double tol,
+                               uint8_t* __restrict__ dropped, int* __restrict__ err) {
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  const i64 col0 = P.sn_col0[g];
+  double* F = fronts + P.sn_fptr[g];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  __shared__ double s_d[64];
+  for (int jj = 0; jj < nb; ++jj) {
+    const int j = j0 + jj;
+    double* Fj = F + (i64)j * nr;
+    const double d = Fj[j];
+    bool drop = false;
+    if (mode == 1) drop = !(d > tol);
+    else if (mode == 2) {
+      if (!(d > tol)) {
+        if (tid == 0) { atomicAdd(err, 1); Fj[j] = tol; }
+        __syncthreads();
+      }
+    } else if (!(d > 0.0)) {
+      if (tid == 0) atomicExch(err, 1);
+      drop = true;
+    }
+    if (drop) {
+      for (int i = j + 1 + tid; i < nr; i += nt) Fj[i] = 0.0;
+      if (tid == 0) {
+        dinv[col0 + j] = 0.0;
+        s_d[jj] = 0.0;
+        if (dropped) dropped[col0 + j] = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    const double dd = Fj[j];
+    const double rd = 1.0 / dd;
+    for (int i = j + 1 + tid; i < nr; i += nt) Fj[i] *= rd;
+    __syncthreads();
+    for (int k = j + 1 + warp; k < j0 + nb; k += nw) {  // the panel's own columns only
+      const double lkd = Fj[k] * dd;
+      double* Fk = F + (i64)k * nr;
+      for (int i = k + lane; i < nr; i += 32) Fk[i] -= Fj[i] * lkd;
+    }
+    if (tid == 0) {
+      dinv[col0 + j] = rd;
+      s_d[jj] = dd;
+      if (dropped) dropped[col0 + j] = 0;
+    }
+    __syncthreads();
+  }
+  const int r0 = j0 + nb, nrest = nr - r0;
+  for (i64 k = tid; k < (i64)nrest * nb; k += nt) {
+    const int jj = (int)(k / nrest), i = (int)(k % nrest);
+    W[k] = F[(i64)(j0 + jj) * nr + r0 + i] * s_d[jj];
+  }
+}
+
+// after the eliminations: L21 into the panel, the update matrix, the unit-lower
+// L11 (strict part from F) into the panel's diagonal block for the in-place
+// triangular inverse
+__global__ void k_front_finish_copy(PlanDev P, int g, const double* __restrict__ fronts, double* __restrict__ L,
+                                    double* __restrict__ umat) {
+  const int nc = P.sn_ncol[g], no = P.sn_noff[g], nr = nc + no;
+  const double* F = fronts + P.sn_fptr[g];
+  double* Lp = L + P.sn_lptr[g];
+  double* U = umat + P.sn_umptr[g];
+  const int tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
+  for (i64 k = tid; k < (i64)nc * nr; k += nt) {
+    const int j = (int)(k / nr), i = (int)(k % nr);
+    Lp[k] = i > j ? F[(i64)j * nr + i] : (i == j ? 1.0 : 0.0);
+  }
+  for (i64 k = tid; k < (i64)no * no; k += nt) {
+    const int b = (int)(k / no), a = (int)(k % no);
+    U[k] = (a >= b) ? F[(i64)(nc + b) * nr + nc + a] : 0.0;
+  }
+}
+
+// D^{-1} folded into the rows of the (inverted) diagonal block
+__global__ void k_front_fold_d(PlanDev P, int g, double* __restrict__ L, const double* __restrict__ dinv) {
+  const int nc = P.sn_ncol[g], nr = nc + P.sn_noff[g];
+  const i64 col0 = P.sn_col0[g];
+  double* Lp = L + P.sn_lptr[g];
+  const int tid = threadIdx.x + blockIdx.x * blockDim.x, nt = blockDim.x * gridDim.x;
   for (i64 k = tid; k < (i64)nc * nc; k += nt) {
     const int j = (int)(k / nc), i = (int)(k % nc);
     if (i >= j) Lp[(i64)j * nr + i] *= dinv[col0 + i];

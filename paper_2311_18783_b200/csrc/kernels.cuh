@@ -83,7 +83,7 @@ struct PlanDev {
 // mode 0: SPD (pivot <= 0 flags an error); mode 1: rank-revealing (pivot <= tol is
 // a dependent column: D^{-1} = 0, L column = 0, flagged in `dropped`); mode 2:
 // static pivoting (pivot <= tol replaced by tol, counted in *err)
-__global__ void k_mf_factor_level(PlanDev P, int level_begin, const double* __restrict__ src,
+__global__ void k_mf_factor_level(PlanDev P, const int* __restrict__ list, const double* __restrict__ src,
                                   double* __restrict__ fronts, double* __restrict__ L,
                                   double* __restrict__ dinv, double* __restrict__ umat, int mode,
                                   double tol, uint8_t* __restrict__ dropped, int* __restrict__ err);
@@ -164,6 +164,20 @@ __global__ void k_sweep(SweepDev S);
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,
                                 const int64_t* __restrict__ lptr);
 
+
+// big fronts: assembly, blocked panel factorisation (trailing updates by cuBLAS),
+// finishing copies and the D^{-1} fold (the triangular inverse and M21 by cuSOLVER /
+// cuBLAS, factor_driver.cu)
+__global__ void k_front_assemble(PlanDev P, int g, const double* __restrict__ src, double* __restrict__ fronts,
+                                 const double* __restrict__ umat);
+__global__ void k_front_assemble2(PlanDev P, int g, const double* __restrict__ src, double* __restrict__ fronts,
+                                  const double* __restrict__ umat);
+__global__ void k_panel_factor(PlanDev P, int g, int j0, int nb, double* __restrict__ fronts,
+                               double* __restrict__ dinv, double* __restrict__ W, int mode, double tol,
+                               uint8_t* __restrict__ dropped, int* __restrict__ err);
+__global__ void k_front_finish_copy(PlanDev P, int g, const double* __restrict__ fronts, double* __restrict__ L,
+                                    double* __restrict__ umat);
+__global__ void k_front_fold_d(PlanDev P, int g, double* __restrict__ L, const double* __restrict__ dinv);
 
 // prolongation sum_i R_i^T x_i: out[e] = sum over the copies of dof e (fixed order)
 __global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
