@@ -201,7 +201,8 @@ struct mdd_solver {
   DBuf<int64_t> Zg_ptr, Zgt_ptr, W_off, W_poff;
   DBuf<int32_t> Zg_idx, Zgt_idx, W_gpos;
   DBuf<double> Zg_val, Zgt_val, W_val, u_loc;
-  DBuf<int> W_n, W_k, W_gc0;
+  DBuf<int> W_n, W_k, W_gc0, W_cblk, W_cnch;
+  DBuf<double> W_part;
   DBuf<int4> W_bzt, W_bz;
   int nbzt = 0, nbz = 0;
   int64_t nnzZg = 0, nnzW = 0;
@@ -267,16 +268,19 @@ struct mdd_solver {
   void apply_coarse(const double* v, double* y) {
     dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, xc.p,
                                               nullptr, nullptr, state.p);
-    if (nbzt)
+    if (nbzt) {
       dev::k_geneo_zt<<<nbzt, 256, 0, stream>>>(W_bzt.p, W_off.p, W_poff.p, W_n.p, W_gc0.p, W_gpos.p, W_val.p,
-                                                gmap.p, v, xc.p, state.p);
+                                                gmap.p, v, W_part.p, state.p);
+      dev::k_geneo_zt2<<<nblk(ngeneo, 128), 128, 0, stream>>>((int)ngeneo, W_cblk.p, W_cnch.p, W_gpos.p,
+                                                              W_part.p, xc.p, state.p);
+    }
     crs.sweep(xc.p, nullptr, stream, state.p);
     if (nbz)
       dev::k_geneo_z<<<nbz, 256, 0, stream>>>(W_bz.p, W_off.p, W_poff.p, W_n.p, W_k.p, W_gc0.p, W_gpos.p,
                                               W_val.p, crs.xb.p, u_loc.p, state.p);
     dev::k_z_apply<<<nparts, 256, 0, stream>>>(n, Zg_ptr.p, Zg_idx.p, Zg_val.p, crs.xb.p, pro_ptr.p, pro_pos.p,
                                               nbz ? u_loc.p : nullptr, y, state.p);
-    launches += 3 + (nbzt ? 1 : 0) + (nbz ? 1 : 0);
+    launches += 3 + (nbzt ? 2 : 0) + (nbz ? 1 : 0);
   }
   void apply_prec(const double* rr, double* zz) {
     int v = desc.variant;
@@ -859,6 +863,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         std::vector<int> nsz(nsub), kc(nsub), gc0(nsub);
         std::vector<int32_t> gpos(H->ngeneo);
         std::vector<int4> bzt, bz;
+        std::vector<int> zt_cblk, zt_cnch;  // per GenEO column, in column order
         int64_t wtot = 0;
         int gcol = 0;
         for (int i = 0; i < nsub; ++i) {
@@ -870,7 +875,18 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
             MDD_REQUIRE(tp[c + 1] - tp[c] == ni, 5, "GenEO column is not dense on its subdomain");
             for (int q = 0; q < ni; ++q) wsrc.push_back(tp[c] + lp.perm[lp.sys_off[i] + q]);
           }
-          for (int k0 = 0; k0 < ki; k0 += 8) bzt.push_back(make_int4(i, k0, std::min(8, ki - k0), 0));
+          // Z_e^T v blocks: (column chunk of 8) x (row chunk of kGeneoRows); the
+          // blocks of one column chunk are consecutive (stage 2 adds them in order)
+          for (int k0 = 0; k0 < ki; k0 += 8) {
+            const int first = (int)bzt.size();
+            int nch = 0;
+            for (int r0 = 0; r0 < ni; r0 += dev::kGeneoRows, ++nch)
+              bzt.push_back(make_int4(i, k0, std::min(8, ki - k0), r0));
+            for (int q = 0; q < std::min(8, ki - k0); ++q) {
+              zt_cblk.push_back(first * 8 + q);
+              zt_cnch.push_back(nch);
+            }
+          }
           if (ki > 0)
             for (int r0 = 0; r0 < ni; r0 += 256) bz.push_back(make_int4(i, r0, 0, 0));
           wtot += (int64_t)ni * ki;
@@ -884,6 +900,9 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         H->W_off.upload(woff); H->W_poff.upload(poff); H->W_n.upload(nsz); H->W_k.upload(kc);
         H->W_gc0.upload(gc0); H->W_gpos.upload(gpos); H->W_bzt.upload(bzt); H->W_bz.upload(bz);
         H->nbzt = (int)bzt.size();
+        H->W_cblk.upload(zt_cblk);
+        H->W_cnch.upload(zt_cnch);
+        H->W_part.alloc((int64_t)H->nbzt * 8);
         H->nbz = (int)bz.size();
         H->u_loc.alloc(lp.ntot);
         // positions of subdomains without GenEO vectors are never written by

@@ -491,27 +491,29 @@ MDD_SPMV_G(k_spmv32, 32)
 #undef MDD_SPMV_G
 
 // ---------------------------------------------------------- GenEO blocks
-// Z_e^T v: y[gpos[c]] = sum_p W_i[p + k n_i] v[gmap[off_i + p]] for the GenEO
-// columns k of subdomain i (tall-skinny reduction, fixed order: per thread a
-// strided row range, then warp shuffles, then the warps in order)
+// Z_e^T v, stage 1: for block b = (subdomain i, columns [k0, k0+kc), rows
+// [r0, r0+rc)): part[b][q] = sum_{p in rows} W_i[p + (k0+q) n_i] v[gmap[off_i + p]]
+// (per thread a strided row range, then warp shuffles, then the warps in order:
+// a fixed reduction order, the stage-2 kernel adds the row chunks in order)
 __global__ void __launch_bounds__(256) k_geneo_zt(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                                                   const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                                                   const int* __restrict__ gcol0, const int32_t* __restrict__ gpos,
                                                   const double* __restrict__ W, const int32_t* __restrict__ gmap,
-                                                  const double* __restrict__ v, double* __restrict__ y,
+                                                  const double* __restrict__ v, double* __restrict__ part,
                                                   const int* __restrict__ stop) {
   if (STOPPED) return;
   constexpr int KC = 8;
   __shared__ double red[8][KC];
-  const int4 b = blk[blockIdx.x];  // {subdomain, first column, columns, -}
-  const int i = b.x, k0 = b.y, kc = b.z;
+  const int4 b = blk[blockIdx.x];  // {subdomain, first column, columns, first row}
+  const int i = b.x, k0 = b.y, kc = b.z, r0 = b.w;
   const int ni = nsz[i];
+  const int r1 = min(ni, r0 + kGeneoRows);
   const double* Wi = W + woff[i] + (int64_t)k0 * ni;
   const int32_t* gm = gmap + poff[i];
   double acc[KC];
 #pragma unroll
   for (int q = 0; q < KC; ++q) acc[q] = 0.0;
-  for (int p = threadIdx.x; p < ni; p += blockDim.x) {
+  for (int p = r0 + threadIdx.x; p < r1; p += blockDim.x) {
     const double vp = v[gm[p]];
 #pragma unroll
     for (int q = 0; q < KC; ++q)
@@ -527,8 +529,23 @@ __global__ void __launch_bounds__(256) k_geneo_zt(const int4* __restrict__ blk, 
   if (threadIdx.x < kc) {
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q][threadIdx.x];
-    y[gpos[gcol0[i] + k0 + threadIdx.x]] = t;
+    part[(int64_t)blockIdx.x * KC + threadIdx.x] = t;
   }
+}
+
+// Z_e^T v, stage 2: y[gpos[c]] = sum of the row-chunk partials of column c, in order
+// (cpart[c] = first block of column c's column chunk, cstride = blocks per row chunk)
+__global__ void k_geneo_zt2(int ncols, const int* __restrict__ cblk, const int* __restrict__ cnch,
+                            const int32_t* __restrict__ gpos, const double* __restrict__ part,
+                            double* __restrict__ y, const int* __restrict__ stop) {
+  if (STOPPED) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  // cblk[c] = (first block of the column's chunk) * 8 + lane within the chunk
+  const int b0 = cblk[c] >> 3, q = cblk[c] & 7;
+  double t = 0.0;
+  for (int r = 0; r < cnch[c]; ++r) t += part[(int64_t)(b0 + r) * 8 + q];
+  y[gpos[c]] = t;
 }
 
 // u[off_i + p] = sum_k W_i[p + k n_i] xc[gpos[gcol0_i + k]]  (rows of subdomain i)
@@ -546,9 +563,16 @@ __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, c
   if (p >= ni) return;
   const double* Wi = W + woff[i];
   const int32_t* gp = gpos + gcol0[i];
-  double s = 0.0;
-  for (int k = 0; k < ki; ++k) s += Wi[(int64_t)k * ni + p] * xc[gp[k]];
-  u[poff[i] + p] = s;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= ki; k += 4) {
+    s0 += Wi[(int64_t)k * ni + p] * xc[gp[k]];
+    s1 += Wi[(int64_t)(k + 1) * ni + p] * xc[gp[k + 1]];
+    s2 += Wi[(int64_t)(k + 2) * ni + p] * xc[gp[k + 2]];
+    s3 += Wi[(int64_t)(k + 3) * ni + p] * xc[gp[k + 3]];
+  }
+  for (; k < ki; ++k) s0 += Wi[(int64_t)k * ni + p] * xc[gp[k]];
+  u[poff[i] + p] = (s0 + s1) + (s2 + s3);
 }
 
 // out[e] = Z_g(e, :) xc + sum of the GenEO contributions u at the copies of e

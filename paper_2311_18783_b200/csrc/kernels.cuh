@@ -198,11 +198,15 @@ MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
 MDD_SPMV_G_DECL(k_spmv32)
 #undef MDD_SPMV_G_DECL
+constexpr int kGeneoRows = 1024;  // rows per block of the Z_e^T v reduction
 __global__ void k_geneo_zt(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                            const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                            const int* __restrict__ gcol0, const int32_t* __restrict__ gpos,
                            const double* __restrict__ W, const int32_t* __restrict__ gmap,
-                           const double* __restrict__ v, double* __restrict__ y, const int* __restrict__ stop);
+                           const double* __restrict__ v, double* __restrict__ part, const int* __restrict__ stop);
+__global__ void k_geneo_zt2(int ncols, const int* __restrict__ cblk, const int* __restrict__ cnch,
+                            const int32_t* __restrict__ gpos, const double* __restrict__ part,
+                            double* __restrict__ y, const int* __restrict__ stop);
 __global__ void k_geneo_z(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                           const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                           const int* __restrict__ kcnt, const int* __restrict__ gcol0,
