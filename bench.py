@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # as2_coarse_start: M_AS,2 (eq. 2.4) with PCG started from x0 = Q f, one coarse
+    # solve per iteration (reading R13); as2: the same operator from x0 = 0
+    ap.add_argument("--variant", default="as2_coarse_start",
+                    choices=["as2_coarse_start", "as2", "additive", "as1"])
     ap.add_argument("--maxit", type=int, default=2000)
     return ap.parse_args()
 
@@ -104,20 +108,21 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_oracle_sample(cfg, max_seconds=30.0, min_solves=1):
+def cpu_oracle_sample(cfg, max_seconds=30.0, min_solves=1, variant="as2_coarse_start"):
     """Time the CPU oracle's solve phase (PCG to 1e-8 with M_AS,2) on the bounded
     sample; returns (DOF*iter/s, description, cores)."""
     import threadpoolctl  # noqa: F401  (scipy/numpy BLAS pools are used as they stand)
     from oracle import solver as osolver
     w = workloads.make(cfg, **CPU_SAMPLE) if cfg in ("c1",) else workloads.make(cfg)
     t0 = time.perf_counter()
-    P = osolver.Problem(w)
+    P = osolver.Problem(w, variant="as2" if variant == "as2_coarse_start" else variant)
+    x0 = "coarse" if variant == "as2_coarse_start" else "zero"
     setup = time.perf_counter() - t0
     f = workloads.rhs(P.n, w.f_seed)
     work, el, solves = 0.0, 0.0, 0
     while solves < min_solves or el < max_seconds * 0.3:
         t0 = time.perf_counter()
-        _, it, _ = P.solve(f, tol=TOL)
+        _, it, _ = P.solve(f, tol=TOL, x0=x0)
         el += time.perf_counter() - t0
         work += P.n * it
         solves += 1
@@ -125,7 +130,8 @@ def cpu_oracle_sample(cfg, max_seconds=30.0, min_solves=1):
             break
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     desc = (f"oracle (numpy/scipy fp64) PCG solve phase on the {cfg} recipe at "
-            f"{w.nx}^3 cubes, {w.px}^3 subdomains (n={P.n}, {it} iterations), {solves} solve(s); "
+            f"{w.nx}^3 cubes, {w.px}^3 subdomains (n={P.n}, {it} iterations, variant {variant}), "
+            f"{solves} solve(s); "
             f"oracle setup {setup:.1f}s untimed")
     return work / el, desc, cores, el / solves
 
@@ -137,7 +143,7 @@ def run_reference(args, rank, world):
     vals = []
     desc = cores = None
     for k in range(args.warmup + args.steps):
-        v, desc, cores, _ = cpu_oracle_sample(cfg, max_seconds=10.0)
+        v, desc, cores, _ = cpu_oracle_sample(cfg, max_seconds=10.0, variant=args.variant)
         if k >= args.warmup:
             vals.append(v)
     v = statistics.median(vals)
@@ -187,7 +193,7 @@ def main():
 
     w = workloads.make(args.config)
     t0 = time.perf_counter()
-    G = MaxwellDD(w, device=local)
+    G = MaxwellDD(w, device=local, variant=args.variant)
     setup_s = time.perf_counter() - t0
     stream = torch.cuda.Stream()
     G.set_stream(stream)
@@ -279,6 +285,26 @@ def main():
     e2e_ms_max, e2e_total = reduce_over_ranks(e2e_ms, e2e_work, world, "cuda")
     e2e_val = e2e_total / (e2e_ms_max / 1e3)
 
+    # ---- the literal eq. (2.4) loop from x0 = 0 beside it (same handle; context)
+    alt = None
+    if args.variant == "as2_coarse_start":
+        G.set_variant("as2")
+        G.solve(f, x, tol=TOL, maxit=args.maxit)
+        a_ms, a_it = 0.0, 0
+        for _ in range(2):
+            l2_flush()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            a_it, _, _ = G.solve(f, x, tol=TOL, maxit=args.maxit)
+            e1.record(stream)
+            e1.synchronize()
+            a_ms += e0.elapsed_time(e1)
+        a_ms /= 2
+        alt = {"variant": "as2 (x0 = 0, two coarse solves per iteration)", "iterations": a_it,
+               "ms_per_step": a_ms, "value": n * a_it / (a_ms / 1e3)}
+        G.set_variant(args.variant)
+
     info = G.info
     roof = roofline(G, sweep_ms, in_step)
     line = {
@@ -288,6 +314,7 @@ def main():
         "config": {"workload": w.name, "n_dofs": n, "subdomains": info["nsub"],
                    "n0_coarse": info["n0"], "geneo_vectors": info["ngeneo"],
                    "iterations": iters[-1], "tol": TOL, "gamma": w.gamma,
+                   "variant": args.variant,
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "flushed between steps (256 MB write)"},
         "iterations": iters[-1],
@@ -295,6 +322,7 @@ def main():
         "setup_s": setup_s,
         "setup_phases_s": G.setup_times(),
         "phase_ms_one_solve_eager": {k: v[0] for k, v in prof.items()},
+        "variant_x0_zero": alt,
         "roofline": roof,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
@@ -302,7 +330,7 @@ def main():
         "clocks": clocks,
     }
     if rank == 0 and not args.no_cpu_baseline:
-        v, desc, cores, _ = cpu_oracle_sample(args.config)
+        v, desc, cores, _ = cpu_oracle_sample(args.config, variant=args.variant)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                 "sample": desc}
     if rank == 0:

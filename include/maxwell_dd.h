@@ -56,6 +56,13 @@ extern "C" {
 #define MDD_VARIANT_AS2 0       /* M_AS,2 = Q + (I - QA) M_AS (I - AQ), eq. (2.4)   */
 #define MDD_VARIANT_ADDITIVE 1  /* M_AS + Q (north_star's written sum, D_i dropped) */
 #define MDD_VARIANT_AS1 2       /* M_AS only                                        */
+/* M_AS,2 again, PCG started from the coarse Galerkin solution x0 = Q f (DESIGN.md
+ * reading R13).  Then Z^T r_k = 0 for all k and eq. (2.4) equals
+ * M_AS r + Q (r - A M_AS r): the PCG loop applies that form (one coarse solve
+ * and one A product per iteration instead of two each).  Same PCG iterates as
+ * MDD_VARIANT_AS2 from x0 = Q f in exact arithmetic; mdd_apply_preconditioner
+ * still applies the full eq. (2.4) operator. */
+#define MDD_VARIANT_AS2_COARSE_START 3
 
 typedef struct mdd_solver* mdd_handle;
 
@@ -103,6 +110,10 @@ int mdd_solve_host(mdd_handle h, const double* f, double* x, double tol, int max
  * replaced); NULL restores a private non-blocking stream.  Synchronises the
  * previous stream first. */
 int mdd_set_stream(mdd_handle h, void* stream);
+/* Switch the preconditioner variant (MDD_VARIANT_*) of an existing handle; the
+ * setup data is shared by all variants.  Variants other than MDD_VARIANT_AS1
+ * need a coarse space (MDD_ERR_ARG otherwise / for an unknown value). */
+int mdd_set_variant(mdd_handle h, int variant);
 
 /* z = M^{-1} r for the configured variant (eq. 2.3 / 2.4).  DEVICE pointers. */
 int mdd_apply_preconditioner(mdd_handle h, const double* r, double* z);
@@ -182,10 +193,10 @@ const char* mdd_phase_name(int phase);
 /* Per-phase device time of the last mdd_solve with profiling enabled, in ms
  * (HOST out[0..MDD_PROF_COUNT)), and the number of launches of each phase. */
 enum {
-  MDD_PROF_SPMV = 0,        /* A p (+ dot)                               */
-  MDD_PROF_LOCAL_FWD,       /* forward+diagonal supernodal solves        */
-  MDD_PROF_LOCAL_BWD,       /* backward supernodal solves                */
-  MDD_PROF_COARSE,          /* Z^T, coarse solves, Z                     */
+  MDD_PROF_SPMV = 0,        /* A p (+ dot) of the PCG iteration          */
+  MDD_PROF_LOCAL,           /* local solves M_AS (the k_sweep launch)    */
+  MDD_PROF_PREC_OTHER,      /* A products + vector ops inside M_AS,2     */
+  MDD_PROF_COARSE,          /* Z^T, coarse solves E^{-1}, Z              */
   MDD_PROF_VECTOR,          /* PCG vector updates, reductions            */
   MDD_PROF_TOTAL,
   MDD_PROF_COUNT

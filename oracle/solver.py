@@ -5,6 +5,11 @@ PAPER.md
 * eq. (2.4)  M_AS,2^{-1} = Z E^{-1} Z^T + (I - P0) M_AS^{-1} (I - P0^T),
              P0 = Z E^{-1} Z^T A  (and the final display of §3),
 * BASELINE north_star: preconditioned CG, stop at relative residual tol.
+* Initial guess (reading R13, the paper does not fix one): x0 = 0, or the
+  coarse-space Galerkin solution x0 = Q f ("coarse").  From x0 = Q f one has
+  Z^T r_k = 0 for every k, so M_AS,2 r_k = (I - Q A) M_AS r_k (the balancing
+  identity of Mandel's BDD; tests/test_oracle_solver.py pins it); the oracle
+  still applies the full eq. (2.4) operator in either case.
 The "additive" variant sum_i R_i^T A_i^{-1} R_i + Z E^{-1} Z^T is north_star's
 written form without D_i (reading R1); it is exposed for comparison only.
 """
@@ -48,15 +53,18 @@ class Schwarz:
         return qr + w - self.q(self.A @ w)
 
 
-def pcg(A, f, M, tol=1e-8, maxit=1000):
-    """Textbook preconditioned CG from x0 = 0; stops when ||r_k|| <= tol ||f||.
-    Returns (x, iterations, relative residual history)."""
-    x = np.zeros_like(f)
-    r = f.copy()
+def pcg(A, f, M, tol=1e-8, maxit=1000, x0=None, callback=None):
+    """Textbook preconditioned CG from x0 (default 0); stops when
+    ||r_k|| <= tol ||f|| (k >= 1).  Returns (x, iterations, relative residual
+    history).  callback(k, x, r) sees every iterate (k = 0 is the start)."""
+    x = np.zeros_like(f) if x0 is None else np.array(x0, dtype=float)
+    r = f - A @ x if x0 is not None else f.copy()
     nf = np.linalg.norm(f)
     hist = [1.0]
     if nf == 0.0:
-        return x, 0, hist
+        return np.zeros_like(f), 0, hist
+    if callback:
+        callback(0, x, r)
     z = M(r)
     p = z.copy()
     rz = r @ z
@@ -67,6 +75,8 @@ def pcg(A, f, M, tol=1e-8, maxit=1000):
         r -= alpha * q
         rel = np.linalg.norm(r) / nf
         hist.append(rel)
+        if callback:
+            callback(k, x, r)
         if rel <= tol:
             return x, k, hist
         z = M(r)
@@ -98,5 +108,9 @@ class Problem:
     def n(self):
         return self.A.shape[0]
 
-    def solve(self, f, tol=1e-8, maxit=1000):
-        return pcg(self.A, f, self.M_inv, tol, maxit)
+    def solve(self, f, tol=1e-8, maxit=1000, x0="zero", callback=None):
+        """PCG with this problem's preconditioner; x0 = "zero" or "coarse" (Q f)."""
+        start = None
+        if x0 == "coarse" and self.cs is not None:
+            start = self.M_inv.q(f)
+        return pcg(self.A, f, self.M_inv, tol, maxit, x0=start, callback=callback)

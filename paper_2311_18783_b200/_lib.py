@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, "libmaxwell_dd.so")
 MDD_OK, MDD_ERR_CUDA, MDD_ERR_ARG, MDD_ERR_NOTPD, MDD_ERR_NOCONV, MDD_ERR_INTERNAL, MDD_ERR_BREAKDOWN = range(7)
 DIRICHLET = {"outer": 0, "all": 1, "none": 2}
 COARSE = {"none": 0, "snk": 1, "nk": 2}
-VARIANT = {"as2": 0, "additive": 1, "as1": 2}
+VARIANT = {"as2": 0, "additive": 1, "as1": 2, "as2_coarse_start": 3}
 
 INFO_NAMES = ["n", "nedges", "nfree_nodes", "nsub", "nnz_A", "nloc", "grad_candidates",
               "grad_rank", "ngeneo", "n0", "local_factor_nnz", "coarse_factor_nnz",
@@ -26,7 +26,7 @@ INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, 
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
               "geneo_count": 10}
 DBL_ARRAYS = {"A_val": 0, "K_val": 1, "M_val": 2, "geneo_lambda": 3, "setup_times": 4}
-PROF_NAMES = ["spmv", "local_fwd", "local_bwd", "coarse", "vector", "total"]
+PROF_NAMES = ["spmv", "local", "prec_other", "coarse", "vector", "total"]
 
 
 class SetupDesc(C.Structure):
@@ -39,7 +39,7 @@ class SetupDesc(C.Structure):
 
 
 # every symbol include/maxwell_dd.h declares (checked by tests/test_abi.py)
-EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_stream",
+EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_stream", "mdd_set_variant",
            "mdd_apply_preconditioner",
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_info",
            "mdd_get_int_array", "mdd_topology_int_array", "mdd_get_double_array",
@@ -60,6 +60,7 @@ def load() -> C.CDLL:
         "mdd_solve": (C.c_int, [P, P, P, C.c_double, C.c_int, C.POINTER(C.c_int), dp]),
         "mdd_solve_host": (C.c_int, [P, dp, dp, C.c_double, C.c_int, C.POINTER(C.c_int), dp]),
         "mdd_set_stream": (C.c_int, [P, P]),
+        "mdd_set_variant": (C.c_int, [P, C.c_int]),
         "mdd_apply_preconditioner": (C.c_int, [P, P, P]),
         "mdd_apply_operator": (C.c_int, [P, P, P]),
         "mdd_apply_local": (C.c_int, [P, P, P]),

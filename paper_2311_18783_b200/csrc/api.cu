@@ -222,6 +222,20 @@ struct mdd_solver {
   double prof_ms[MDD_PROF_COUNT] = {0};
   int64_t prof_launch[MDD_PROF_COUNT] = {0};
   cudaEvent_t ev[16];
+  // eager profiling: event pairs around the local / coarse applications of one
+  // iteration (ev[7..15]); nullptr outside the profiling path
+  std::vector<std::pair<int, int>>* prof_pairs = nullptr;
+  int prof_next = 7;
+  void prof_begin(int phase) {
+    if (!prof_pairs || prof_next + 1 >= 16) return;
+    CUDA_CHECK(cudaEventRecord(ev[prof_next], stream));
+    prof_pairs->push_back({phase, prof_next});
+    prof_next += 2;
+  }
+  void prof_end() {
+    if (!prof_pairs || prof_pairs->empty()) return;
+    CUDA_CHECK(cudaEventRecord(ev[prof_pairs->back().second + 1], stream));
+  }
   // CUDA graph of the whole solve: prologue + device-side WHILE loop over iterations
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t graph_stream = nullptr;
@@ -260,12 +274,15 @@ struct mdd_solver {
   // z = sum_i R_i^T A_i^{-1} R_i r: one persistent launch (gather, fwd, D^{-1}, bwd,
   // prolongation)
   void apply_local(const double* rr, double* zz) {
+    prof_begin(MDD_PROF_LOCAL);
     loc.sweep(rr, zz, stream, state.p);
+    prof_end();
     launches += 1;
   }
   // y = Z E^{-1} Z^T v: Z_g^T v (CSR) and Z_e^T v (tall-skinny over the GenEO blocks),
   // the sweep on E, then Z_g xc + prolongation of the GenEO blocks' W_i xc_i
   void apply_coarse(const double* v, double* y) {
+    prof_begin(MDD_PROF_COARSE);
     dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, xc.p,
                                               nullptr, nullptr, state.p);
     if (nbzt) {
@@ -280,6 +297,7 @@ struct mdd_solver {
                                               W_val.p, crs.xb.p, u_loc.p, state.p);
     dev::k_z_apply<<<nparts, 256, 0, stream>>>(n, Zg_ptr.p, Zg_idx.p, Zg_val.p, crs.xb.p, pro_ptr.p, pro_pos.p,
                                               nbz ? u_loc.p : nullptr, y, state.p);
+    prof_end();
     launches += 3 + (nbzt ? 2 : 0) + (nbz ? 1 : 0);
   }
   void apply_prec(const double* rr, double* zz) {
@@ -305,6 +323,21 @@ struct mdd_solver {
     dev::k_combine3<<<nblk(n, 256), 256, 0, stream>>>(n, t1.p, t4.p, t3.p, zz, state.p);
     launches += 2;  // axpby + combine3
   }
+  bool coarse_start() const { return has_coarse && desc.variant == MDD_VARIANT_AS2_COARSE_START; }
+  // the preconditioner inside the PCG loop: for the coarse start (Z^T r = 0,
+  // reading R13) eq. (2.4) is z = w + Q (r - A w), w = M_AS r
+  void apply_prec_loop(const double* rr, double* zz) {
+    if (!coarse_start()) {
+      apply_prec(rr, zz);
+      return;
+    }
+    apply_local(rr, t4.p);                                         // w = M_AS r
+    applyA(t4.p, t2.p);                                            // A w
+    dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, rr, -1.0, t2.p, t3.p, state.p);  // r - A w
+    apply_coarse(t3.p, t1.p);                                      // Q (r - A w)
+    dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, t4.p, 1.0, t1.p, zz, state.p);
+    launches += 2;
+  }
   void check_aborts() {
     loc.check_abort(stream);
     if (has_coarse) crs.check_abort(stream);
@@ -323,7 +356,15 @@ struct mdd_solver {
   void enqueue_prologue() {
     dot(r.p, r.p, dev::S_RR);
     scalar(3);
-    apply_prec(r.p, z.p);
+    if (coarse_start()) {
+      // x0 = Q f, r0 = f - A x0 (the staged x is 0; reading R13)
+      apply_coarse(r.p, x.p);
+      applyA(x.p, t2.p);
+      dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, r.p, -1.0, t2.p, t3.p, state.p);
+      dev::k_copy<<<nblk(n, 256), 256, 0, stream>>>(n, t3.p, r.p, state.p);
+      launches += 2;
+    }
+    apply_prec_loop(r.p, z.p);
     dev::k_copy<<<nblk(n, 256), 256, 0, stream>>>(n, z.p, p.p, state.p);
     launches += 1;
     dot(r.p, z.p, dev::S_RZ);
@@ -342,7 +383,7 @@ struct mdd_solver {
     launches += 2;
     scalar(1);
     if (mark) mark(4);
-    apply_prec(r.p, z.p);
+    apply_prec_loop(r.p, z.p);
     if (mark) mark(5);
     dot(r.p, z.p, dev::S_RZNEW);
     scalar(2);
@@ -402,7 +443,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
   MDD_REQUIRE(d->gamma > 0, 2, "gamma must be > 0");
   MDD_REQUIRE(d->mu_inv && d->eps, 2, "coefficients required");
   MDD_REQUIRE(d->coarse_kind >= 0 && d->coarse_kind <= 2, 2, "bad coarse kind");
-  MDD_REQUIRE(d->variant >= 0 && d->variant <= 2, 2, "bad variant");
+  MDD_REQUIRE(d->variant >= 0 && d->variant <= 3, 2, "bad variant");
   H->desc = *d;
   H->desc.cube_mask = nullptr;
   H->desc.mu_inv = H->desc.eps = nullptr;
@@ -978,13 +1019,25 @@ void solve_impl(mdd_solver* H, const double* f, double* x, double tol, int maxit
     };
     H->launches = 0;
     H->enqueue_prologue();
+    std::vector<std::pair<int, int>> pairs;
     for (int k = 1; k <= std::max(maxit, 1); ++k) {
+      pairs.clear();
+      H->prof_pairs = &pairs;
+      H->prof_next = 7;
       H->enqueue_body(mark);
+      H->prof_pairs = nullptr;
       CUDA_CHECK(cudaMemcpyAsync(H->host_state, H->state.p, ST_COUNT * sizeof(int), cudaMemcpyDeviceToHost, s));
       CUDA_CHECK(cudaStreamSynchronize(s));
       acc(MDD_PROF_SPMV, 2, 3);
       acc(MDD_PROF_VECTOR, 3, 4);
-      acc(MDD_PROF_LOCAL_FWD, 4, 5);  // the whole preconditioner application
+      acc(MDD_PROF_PREC_OTHER, 4, 5);  // the whole preconditioner application ...
+      for (auto& pr : pairs) {          // ... minus its local and coarse parts
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev[pr.second], ev[pr.second + 1]));
+        H->prof_ms[pr.first] += ms;
+        H->prof_launch[pr.first] += 1;
+        H->prof_ms[MDD_PROF_PREC_OTHER] -= ms;
+      }
       acc(MDD_PROF_VECTOR, 5, 6);
       acc(MDD_PROF_TOTAL, 2, 6);
       if (H->host_state[ST_STOP]) break;
@@ -1061,6 +1114,19 @@ int mdd_set_stream(mdd_handle h, void* stream) {
       CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
       h->own_stream = true;
     }
+  });
+}
+
+int mdd_set_variant(mdd_handle h, int variant) {
+  if (!h) { g_err = "null argument"; return MDD_ERR_ARG; }
+  if (variant < 0 || variant > MDD_VARIANT_AS2_COARSE_START) { g_err = "bad variant"; return MDD_ERR_ARG; }
+  return guard([&] {
+    MDD_REQUIRE(h->has_coarse || variant == MDD_VARIANT_AS1, 2,
+                "variant needs a coarse space (the handle was set up with MDD_COARSE_NONE)");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    h->drop_graph();
+    h->desc.variant = variant;
   });
 }
 

@@ -127,6 +127,12 @@ class MaxwellDD:
         raw = None if stream is None else int(getattr(stream, "cuda_stream", stream))
         L.check(L.lib().mdd_set_stream(self._h, raw))
 
+    def set_variant(self, variant: str):
+        """Switch the preconditioner variant ("as2", "as2_coarse_start",
+        "additive", "as1") without redoing the setup."""
+        L.check(L.lib().mdd_set_variant(self._h, L.VARIANT[variant]))
+        self.variant = variant
+
     def last_launches(self):
         return int(self._info()["last_launches"])
 

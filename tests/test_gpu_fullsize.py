@@ -96,6 +96,28 @@ def test_pcg_full_size(c1):
     assert it2 == it and np.array_equal(x.cpu().numpy(), xh)   # bit-reproducible
 
 
+def test_pcg_full_size_coarse_start(c1):
+    """Reading R13 at full size: the one-coarse-solve loop from x0 = Q f takes the
+    iteration count of eq. (2.4) from x0 = 0 (+-1), reaches the same true
+    residual level and is bit-reproducible."""
+    w, G, A, dec = c1
+    f = workloads.rhs(A.shape[0], w.f_seed)
+    x = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    it0, _, _ = G.solve(dev(f), x, tol=1e-8)
+    x0 = x.cpu().numpy()
+    G.set_variant("as2_coarse_start")
+    try:
+        it, rel, ok = G.solve(dev(f), x, tol=1e-8)
+        xh = x.cpu().numpy()
+        it2, _, _ = G.solve(dev(f), x, tol=1e-8)
+        assert it2 == it and np.array_equal(x.cpu().numpy(), xh)
+    finally:
+        G.set_variant("as2")
+    assert ok and rel <= 1e-8 and abs(it - it0) <= 1
+    assert np.linalg.norm(f - A @ xh) <= 1e-3 * np.linalg.norm(f)
+    assert np.linalg.norm(xh - x0) <= 1e-4 * np.linalg.norm(x0)
+
+
 def test_sweep_is_grid_independent_and_reproducible():
     # the persistent sweep's partial sums are combined in a fixed order, so the
     # result must not depend on how many CTAs run it (a race or a shared-memory

@@ -76,7 +76,8 @@ def pair(name, coarse="snk", variant="as2"):
         from paper_2311_18783_b200 import MaxwellDD
         w = CASES[name]()
         P = osolver.Problem(w, kind=coarse if coarse != "none" else "snk",
-                            variant=variant, coarse_on=coarse != "none")
+                            variant="as2" if variant == "as2_coarse_start" else variant,
+                            coarse_on=coarse != "none")
         G = MaxwellDD(w, coarse=coarse, variant=variant)
         _cache[key] = (w, P, G)
     return _cache[key]
@@ -156,6 +157,31 @@ def test_pcg_parity(name):
     assert ith == it and np.array_equal(xh, host(x))   # deterministic
 
 
+@pytest.mark.parametrize("name", list(CASES))
+def test_pcg_coarse_start_parity(name):
+    """Reading R13: the device loop applies M_AS r + Q (r - A M_AS r) from
+    x0 = Q f; the oracle runs textbook PCG with the full eq. (2.4) operator from
+    the same start.  Same tolerances as test_pcg_parity."""
+    w, P, G = pair(name, variant="as2_coarse_start")
+    f = workloads.rhs(P.n, w.f_seed)
+    xo, ito, _ = P.solve(f, tol=1e-8, x0="coarse")
+    x = torch.empty(P.n, dtype=torch.float64, device="cuda")
+    it, relres, ok = G.solve(dev(f), x, tol=1e-8)
+    assert ok and relres <= 1e-8
+    assert abs(it - ito) <= 1
+    assert rel(host(x), xo) <= tol_for(P, 1e-8, "global")
+    tr_g = np.linalg.norm(f - P.A @ host(x)) / np.linalg.norm(f)
+    tr_o = np.linalg.norm(f - P.A @ xo) / np.linalg.norm(f)
+    assert tr_g <= max(2 * tr_o, 1e-8)
+    # the standalone preconditioner is still the full eq. (2.4) operator
+    r = np.random.default_rng(3).standard_normal(P.n)
+    z = torch.empty(P.n, dtype=torch.float64, device="cuda")
+    G.apply_preconditioner(dev(r), z)
+    assert rel(host(z), P.M_inv(r)) <= tol_for(P, 1e-10, "global")
+    xh, ith, _ = G.solve_host(f, tol=1e-8)
+    assert ith == it and np.array_equal(xh, host(x))
+
+
 def test_one_level_and_nk_variants():
     for coarse, variant in [("none", "as1"), ("nk", "as2")]:
         w, P, G = pair("c0", coarse=coarse, variant=variant)
@@ -176,3 +202,22 @@ def test_zero_rhs_and_single_subdomain():
     f = workloads.rhs(G.n, 3)
     it, relres, ok = G.solve(dev(f), x, tol=1e-10)
     assert ok and it == 1
+
+
+def test_profiled_eager_solve_matches_graph_solve():
+    """The eager profiling path (per-phase events) launches the same kernels in the
+    same order as the CUDA graph: identical iterates, and its phases add up."""
+    w, P, G = pair("c0")
+    f = workloads.rhs(P.n, w.f_seed)
+    xg, itg, _ = G.solve_host(f, tol=1e-8)
+    G.set_profiling(True)
+    try:
+        xe, ite, _ = G.solve_host(f, tol=1e-8)
+        prof = G.profile()
+    finally:
+        G.set_profiling(False)
+    assert ite == itg and np.array_equal(xe, xg)
+    parts = sum(prof[k][0] for k in ("spmv", "local", "prec_other", "coarse", "vector"))
+    assert prof["total"][0] > 0 and abs(parts - prof["total"][0]) <= 0.05 * prof["total"][0] + 1e-3
+    assert prof["local"][1] in (ite, ite + 1) and prof["coarse"][1] == 2 * prof["local"][1]
+    assert min(prof[k][0] for k in ("local", "coarse")) > 0 and prof["prec_other"][0] >= 0

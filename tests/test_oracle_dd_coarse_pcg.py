@@ -229,3 +229,62 @@ def test_c0_geneo_empty_like_table1():
     _, it2, _ = P.solve(f)
     _, it1, _ = solver.pcg(P.A, f, solver.Schwarz(P.A, P.dec, None, "as1"))
     assert it2 < it1
+
+
+def test_coarse_start_balancing_identity():
+    """Reading R13, the algebra.  For a Z-orthogonal residual (Z^T r = 0, which
+    PCG keeps for every k from x0 = Q f) Q r = 0, and eq. (2.4) equals both
+    (I - Q A) M_AS r and the one-coarse-solve form M_AS r + Q (r - A M_AS r).
+    On c0 (E well conditioned) the three agree to rounding; on a generic r they
+    do not (the identity needs the start)."""
+    P = solver.Problem(workloads.make("c0"))
+    M = P.M_inv
+    rng = np.random.default_rng(12)
+    v = rng.standard_normal(P.n)
+    r = v - P.A @ M.q(v)                           # Z^T r = 0
+    Z = P.cs.Z @ P.cs.basis
+    assert np.linalg.norm(Z.T @ r) <= 1e-10 * np.linalg.norm(Z.T @ v)
+    full = M(r)
+    w = M.m_as(r)
+    one_solve = w + M.q(r - P.A @ w)
+    reduced = w - M.q(P.A @ w)
+    assert np.linalg.norm(one_solve - full) <= 1e-11 * np.linalg.norm(full)
+    # without the +Q r term the rounding left in Z^T r (~1e-12) is not corrected
+    # but amplified by the local solves: agreement only to ~1e-8 even on c0
+    assert np.linalg.norm(reduced - full) <= 1e-6 * np.linalg.norm(full)
+    wv = M.m_as(v)
+    assert np.linalg.norm(wv + M.q(v - P.A @ wv) - M(v)) > 1e-7 * np.linalg.norm(M(v))
+
+
+def test_coarse_start_trajectory(c1small):
+    """Reading R13 on the contrast-1e4 / gamma-1e-4 recipe (kappa(E) ~ 1e11):
+    PCG with eq. (2.4) from x0 = Q f, from x0 = 0, and with the one-coarse-solve
+    form M_AS r + Q (r - A M_AS r) from x0 = Q f take the same number of
+    iterations and reach the same solution (the form without the +Q r term
+    would stall here: rounding leaves Z^T r_k ~ 1e-8, amplified by E^{-1})."""
+    P = c1small
+    M = P.M_inv
+    f = workloads.rhs(P.n, 11)
+    xz, itz, _ = P.solve(f)
+    xc, itc, hc = P.solve(f, x0="coarse")
+
+    def one_solve(r):
+        w = M.m_as(r)
+        return w + M.q(r - P.A @ w)
+
+    xa, ita, ha = solver.pcg(P.A, f, one_solve, x0=M.q(f))
+    assert hc[-1] <= 1e-8 and ha[-1] <= 1e-8
+    assert abs(itc - itz) <= 1 and abs(ita - itc) <= 1
+    assert np.linalg.norm(xa - xc) <= 1e-8 * np.linalg.norm(xc)
+    # different starts: both residuals <= 1e-8, forward errors differ (~1e-6 here)
+    assert np.linalg.norm(xc - xz) <= 1e-5 * np.linalg.norm(xz)
+
+
+def test_pcg_coarse_start_matches_dense_direct_solve():
+    w = workloads.custom(4, 4, 4, 2, 2, 1, overlap=1, gamma=1e-2, f_seed=5)
+    P = solver.Problem(w)
+    f = workloads.rhs(P.n, 5)
+    x, it, hist = P.solve(f, tol=1e-12, x0="coarse")
+    xd = np.linalg.solve(P.A.toarray(), f)
+    assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
+    assert hist[-1] <= 1e-12
