@@ -810,11 +810,29 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     }
     H->setup_times[PH_COARSE_E] = now_s() - t0;
     t0 = now_s();
-    // GenEO columns (dense support on a whole subdomain) are eliminated last
+    // GenEO columns (dense support on a whole subdomain) are kept out of the
+    // dissection: each closes the smallest subtree whose box holds its coupling
+    // region (the subdomain grown by the overlap and one more cell), or, with
+    // MDD_GENEO_PLACE=last, the whole order
     std::vector<uint8_t> elast(nb, 0);
     for (int64_t c = H->grad_rank; c < nb; ++c) elast[c] = 1;
+    std::vector<int32_t> ebox(6 * nb, 0);
+    {
+      int64_t col = H->grad_rank;
+      const int sx = m.nx / d->px, sy = m.ny / d->py, sz = m.nz / d->pz, g = d->overlap + 1;
+      for (int i = 0; i < nsub; ++i) {
+        int si = i % d->px, sj = (i / d->px) % d->py, sk = i / (d->px * d->py);
+        for (int kk = 0; kk < geneo[i].k; ++kk, ++col) {
+          int32_t* b = &ebox[6 * col];
+          b[0] = 2 * (si * sx - g); b[1] = 2 * (sj * sy - g); b[2] = 2 * (sk * sz - g);
+          b[3] = 2 * ((si + 1) * sx + g); b[4] = 2 * ((sj + 1) * sy + g); b[5] = 2 * ((sk + 1) * sz + g);
+        }
+      }
+    }
     SymSystem esys{&epat, exyz.data(), eslot.data()};
     esys.last = elast.data();
+    const char* place = getenv("MDD_GENEO_PLACE");
+    if (!(place && std::string(place) == "last")) esys.box = ebox.data();
     std::vector<SymSystem> sys{esys};
     build_factor_plan(H->crs.fp, sys, env_int("MDD_ND_LEAF", 64));
     H->crs.name = "coarse";

@@ -96,6 +96,10 @@ struct SymSystem {
   const int32_t* xyz2;                  // 3 ints per unknown: doubled lattice coordinates
   const i64* val_slot;                  // per pattern entry: index of its value in the source array
   const uint8_t* last = nullptr;        // optional: unknowns ordered after the nested dissection
+  // optional, with `last`: per unknown 6 ints (lo xyz, hi xyz, doubled coordinates)
+  // bounding its coupling region; a flagged unknown then closes the smallest
+  // dissection subtree whose box contains that region instead of the whole order
+  const int32_t* box = nullptr;
 };
 
 void build_factor_plan(FactorPlan& fp, const std::vector<SymSystem>& systems, int leaf_size);

@@ -98,6 +98,8 @@ constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 32768;   // stored entries of a supernode one CTA sweeps alone
 constexpr int kStages = 2;       // tile ring slots per CTA (one tile streams while one computes)
 constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can span)
+constexpr int kDescAhead = 4;    // M-task descriptors streamed ahead of the current task
+constexpr int kDescRing = 8;     // descriptor ring slots (> kDescAhead)
 constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
 
 // one task of an M phase (factor_driver.cu builds them, forward and backward)

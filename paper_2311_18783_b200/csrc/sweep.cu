@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   double* const vec2 = vbase + kVecSlots * (kVecMax + 2);  // kVecMax: accumulators
   double* const red = vec2 + kVecMax;                       // kSweepThreads
   __shared__ __align__(8) uint64_t mbar[kStages];
-  __shared__ __align__(16) MTaskDesc s_desc[4];
+  __shared__ __align__(16) MTaskDesc s_desc[kDescRing];
   __shared__ int s_tinfo[kStages];
   __shared__ int s_flag;
   const int tid = threadIdx.x;
@@ -311,46 +311,55 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           const int kt = task_of(i);
           if (kt >= 0)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(
-                             reinterpret_cast<const int4*>(&s_desc[i & 3]) + tid)),
+                             reinterpret_cast<const int4*>(&s_desc[i % kDescRing]) + tid)),
                          "l"(reinterpret_cast<const int4*>(MT + kt) + tid)
                          : "memory");
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
       };
-      desc_fetch(0);
-      desc_fetch(1);
-      desc_fetch(2);
+      for (int q = 0; q < kDescAhead; ++q) desc_fetch(q);
       if (tid < kDW) asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();
       // thread 0's prefetch cursor over this CTA's tile stream (task pi, tile pk);
-      // it runs at most kStages tiles ahead, i.e. <= 2 tasks past the current one
-      int pi = 0, pk = 0, pk1 = 0, ps = 0;
-      auto cursor_load = [&]() {
-        if (task_of(pi) >= 0) { pk = s_desc[pi & 3].k0; pk1 = s_desc[pi & 3].k1; }
-        else pk = pk1 = 0;
-      };
-      auto issue_next = [&]() {  // thread 0
-        if (pk >= pk1) return;
-        const MTaskDesc& Dp = s_desc[pi & 3];
+      // it runs at most kStages tiles ahead, i.e. <= 2 tasks past the current one.
+      // It only moves to a task whose descriptor is known to be resident (task
+      // index <= avail = current + kDescAhead - 1 after the wait below); a ring slot freed
+      // before that is owed and refilled at the next task's start.
+      int pi = -1, pk = 0, pk1 = 0, ps = 0, avail = kDescAhead - 1, owed = 0;
+      auto issue_next = [&]() {  // thread 0: one ring slot is free
+        while (pk >= pk1) {
+          if (task_of(pi + 1) < 0) return;        // stream exhausted
+          if (pi + 1 > avail) { ++owed; return; }  // descriptor not resident yet
+          ++pi;
+          pk = s_desc[pi % kDescRing].k0;
+          pk1 = s_desc[pi % kDescRing].k1;
+        }
+        const MTaskDesc& Dp = s_desc[pi % kDescRing];
         const bool first = pk == Dp.k0;
         prefetch(pk, ps % kStages, Dp.vlo2, first ? Dp.vbytes : 0, pi % kVecSlots);
         ++ps;
-        if (++pk >= pk1) { ++pi; cursor_load(); }
+        ++pk;
       };
-      if (tid == 0) {
-        cursor_load();
+      if (tid == 0)
         for (int q = 0; q < kStages; ++q) issue_next();
-      }
       int cs = 0;  // tiles consumed in this phase
       for (int i = 0;; ++i) {
         const int k = task_of(i);
         if (k < 0) break;
         // descriptors i+1, i+2 must be resident before the cursor reaches them;
         // task i+3's starts streaming now
-        desc_fetch(i + 3);
+        desc_fetch(i + kDescAhead);
         if (tid < kDW) asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        const MTaskDesc D = s_desc[i & 3];
+        if (tid == 0) {
+          avail = i + kDescAhead - 1;
+          for (int q = owed; q > 0; --q) {
+            owed = 0;
+            issue_next();
+            if (owed) { owed = q; break; }
+          }
+        }
+        const MTaskDesc D = s_desc[i % kDescRing];
         const double* const vv = vbase + (i % kVecSlots) * (kVecMax + 2) + D.voff;  // this task's vector
         int buf = 0;
         // wait for the next tile of the stream (its ring slot becomes `buf`)
@@ -447,22 +456,35 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           }
           __syncthreads();
           if (s_flag) {
-            // last tile of its row block (fwd) / column block (bwd): fixed-order combine
-            if (fwd) {
-              const double* fb = S.fpart + D.comb;
-              for (int i2 = tid; i2 < D.rows; i2 += kSweepThreads) {
-                double sum = 0.0;
-                for (int q = 0; q < D.ntl; ++q) sum += __ldcg(fb + (i64)q * D.nr + i2);
-                const int r = D.rb * D.RB + i2;
-                if (r < D.nc) S.xf[D.col0 + r] = sum;
-                else S.upd[D.uptr + (r - D.nc)] = __ldcg(S.vb + D.vo + r) - sum;
+            // last group of its row block (fwd) / column block (bwd): combine the
+            // ntl partials, Lq lanes per output (lane s sums partials s, s+Lq, ...,
+            // then a shuffle tree): a fixed order that depends on ntl only
+            const int m = fwd ? D.rows : D.cols;
+            const int Lq = m <= 32 ? 8 : m <= 64 ? 4 : m <= 128 ? 2 : 1;
+            const double* pb = fwd ? S.fpart + D.comb : S.bpart + D.comb;
+            const i64 ld = fwd ? D.nr : D.nc;
+            const int sub = tid & (Lq - 1);
+            for (int o0 = 0; o0 < m; o0 += kSweepThreads / Lq) {
+              const int o = o0 + tid / Lq;
+              double s0 = 0.0, s1 = 0.0;
+              if (o < m) {
+                int q = sub;
+                for (; q + Lq < D.ntl; q += 2 * Lq) {
+                  s0 += __ldcg(pb + (i64)q * ld + o);
+                  s1 += __ldcg(pb + (i64)(q + Lq) * ld + o);
+                }
+                if (q < D.ntl) s0 += __ldcg(pb + (i64)q * ld + o);
               }
-            } else {
-              const double* bb = S.bpart + D.comb;
-              for (int j = tid; j < D.cols; j += kSweepThreads) {
-                double sum = 0.0;
-                for (int q = 0; q < D.ntl; ++q) sum += __ldcg(bb + (i64)q * D.nc + j);
-                S.xb[D.col0 + D.cb * D.CB + j] = sum;
+              double sum = s0 + s1;
+              for (int w = 1; w < Lq; w <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, w);
+              if (o < m && sub == 0) {
+                if (fwd) {
+                  const int r = D.rb * D.RB + o;
+                  if (r < D.nc) S.xf[D.col0 + r] = sum;
+                  else S.upd[D.uptr + (r - D.nc)] = __ldcg(S.vb + D.vo + r) - sum;
+                } else {
+                  S.xb[D.col0 + D.cb * D.CB + o] = sum;
+                }
               }
             }
           }

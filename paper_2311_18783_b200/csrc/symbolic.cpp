@@ -29,17 +29,25 @@ namespace {
 struct NDWork {
   const Csr* pat;
   const int32_t* xyz2;
+  const int32_t* box = nullptr;  // deferred unknowns' coupling boxes (SymSystem::box)
   std::vector<int32_t> side;   // per vertex: -1 not in current set, 0 left, 1 right, 2 sep
   std::vector<int32_t> order;  // output: new -> old
   int leaf;
 };
 
-void nd_rec(NDWork& w, std::vector<int32_t>& V) {
+// V: unknowns to dissect; T: deferred unknowns whose coupling box lies inside
+// this subtree's region (ordered after the subtree's separator)
+void nd_rec(NDWork& w, std::vector<int32_t>& V, std::vector<int32_t>& T) {
   const size_t nv = V.size();
-  if (nv == 0) return;
+  auto close = [&]() {
+    std::sort(T.begin(), T.end());
+    w.order.insert(w.order.end(), T.begin(), T.end());
+  };
+  if (nv == 0) { close(); return; }
   if ((int)nv <= w.leaf) {
     std::sort(V.begin(), V.end());
     w.order.insert(w.order.end(), V.begin(), V.end());
+    close();
     return;
   }
   int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
@@ -87,13 +95,33 @@ void nd_rec(NDWork& w, std::vector<int32_t>& V) {
   if (!done) {  // cannot split geometrically: dense leaf
     std::sort(V.begin(), V.end());
     w.order.insert(w.order.end(), V.begin(), V.end());
+    close();
     return;
   }
+  // deferred unknowns strictly on one side of the cut plane go down with it
+  std::vector<int32_t> TL, TR, TS;
+  int plane = 0;
+  if (!T.empty()) {
+    // the cut value: the largest L coordinate + 1 .. smallest R coordinate - 1
+    int lmax = INT32_MIN, rmin = INT32_MAX;
+    for (int32_t v : L) lmax = std::max(lmax, w.xyz2[3 * v + axis]);
+    for (int32_t v : R) rmin = std::min(rmin, w.xyz2[3 * v + axis]);
+    plane = L.empty() ? rmin - 1 : lmax + 1;
+    for (int32_t t : T) {
+      const int32_t* b = w.box + 6 * t;
+      if (b[3 + axis] < plane && !L.empty()) TL.push_back(t);
+      else if (b[axis] > std::max(plane, rmin - 1) && !R.empty()) TR.push_back(t);
+      else TS.push_back(t);
+    }
+    std::vector<int32_t>().swap(T);
+  }
   std::vector<int32_t>().swap(V);
-  nd_rec(w, L);
-  nd_rec(w, R);
+  nd_rec(w, L, TL);
+  nd_rec(w, R, TR);
   std::sort(S.begin(), S.end());
   w.order.insert(w.order.end(), S.begin(), S.end());
+  std::sort(TS.begin(), TS.end());
+  w.order.insert(w.order.end(), TS.begin(), TS.end());
 }
 
 // elimination tree of the symmetric matrix P A P^T (Liu); pattern given in the new numbering
@@ -130,14 +158,19 @@ void analyse_one(Sys1& s, const SymSystem& sys, int leaf) {
   const int n = A.nrows;
   s.n = n;
   NDWork w;
-  w.pat = &A; w.xyz2 = sys.xyz2; w.leaf = leaf;
+  w.pat = &A; w.xyz2 = sys.xyz2; w.leaf = leaf; w.box = sys.box;
   w.side.assign(n, -1);
-  std::vector<int32_t> V, tail;
+  std::vector<int32_t> V, tail, none;
   for (int v = 0; v < n; ++v) (sys.last && sys.last[v] ? tail : V).push_back(v);
-  nd_rec(w, V);
-  // flagged unknowns (e.g. dense-support coarse columns) close the order, so their
-  // coupling never creates a clique inside the dissection
-  w.order.insert(w.order.end(), tail.begin(), tail.end());
+  if (sys.box) {
+    // flagged unknowns close the smallest subtree containing their coupling box
+    nd_rec(w, V, tail);
+  } else {
+    // flagged unknowns (e.g. dense-support coarse columns) close the order, so
+    // their coupling never creates a clique inside the dissection
+    nd_rec(w, V, none);
+    w.order.insert(w.order.end(), tail.begin(), tail.end());
+  }
   MDD_REQUIRE((int)w.order.size() == n, 5, "nested dissection lost vertices");
   std::vector<int32_t> perm = w.order, iperm(n);
   // etree + postorder, twice (the second pass is a no-op relabel check)

@@ -140,5 +140,5 @@ def test_sweep_is_grid_independent_and_reproducible():
         G.apply_preconditioner(v, y[2])
         outs[grid] = [t.cpu().numpy() for t in y]
         G.close()
-    for a, b in zip(outs["0"], outs["5"]):
-        assert np.array_equal(a, b)
+    for name, a, b in zip(("local", "coarse", "preconditioner"), outs["0"], outs["5"]):
+        assert np.array_equal(a, b), f"{name}: max rel diff {np.abs(a - b).max() / np.abs(a).max():.3e}"
