@@ -513,11 +513,27 @@ __global__ void __launch_bounds__(256) k_geneo_zt(const int4* __restrict__ blk, 
   double acc[KC];
 #pragma unroll
   for (int q = 0; q < KC; ++q) acc[q] = 0.0;
-  for (int p = r0 + threadIdx.x; p < r1; p += blockDim.x) {
-    const double vp = v[gm[p]];
+  // kGeneoRows / 256 rows per thread: every gather and W load of the chunk is
+  // issued before the first multiply (memory-level parallelism)
+  constexpr int RPT = kGeneoRows / 256;
+  double vp[RPT];
 #pragma unroll
-    for (int q = 0; q < KC; ++q)
-      if (q < kc) acc[q] += Wi[(int64_t)q * ni + p] * vp;
+  for (int t = 0; t < RPT; ++t) {
+    const int p = r0 + t * 256 + (int)threadIdx.x;
+    vp[t] = p < r1 ? __ldg(v + __ldg(gm + p)) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < KC; ++q) {
+    if (q < kc) {
+      double w[RPT];
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int p = r0 + t * 256 + (int)threadIdx.x;
+        w[t] = p < r1 ? __ldcs(Wi + (int64_t)q * ni + p) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) acc[q] += w[t] * vp[t];
+    }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -563,16 +579,21 @@ __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, c
   if (p >= ni) return;
   const double* Wi = W + woff[i];
   const int32_t* gp = gpos + gcol0[i];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  // eight independent column streams in flight per thread
+  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int k = 0;
-  for (; k + 4 <= ki; k += 4) {
-    s0 += Wi[(int64_t)k * ni + p] * xc[gp[k]];
-    s1 += Wi[(int64_t)(k + 1) * ni + p] * xc[gp[k + 1]];
-    s2 += Wi[(int64_t)(k + 2) * ni + p] * xc[gp[k + 2]];
-    s3 += Wi[(int64_t)(k + 3) * ni + p] * xc[gp[k + 3]];
+  for (; k + 8 <= ki; k += 8) {
+    double w[8], x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      w[j] = __ldcs(Wi + (int64_t)(k + j) * ni + p);
+      x[j] = __ldg(xc + __ldg(gp + k + j));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] += w[j] * x[j];
   }
-  for (; k < ki; ++k) s0 += Wi[(int64_t)k * ni + p] * xc[gp[k]];
-  u[poff[i] + p] = (s0 + s1) + (s2 + s3);
+  for (int j = 0; k < ki; ++k, ++j) s[j] += __ldcs(Wi + (int64_t)k * ni + p) * __ldg(xc + __ldg(gp + k));
+  u[poff[i] + p] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 // out[e] = Z_g(e, :) xc + sum of the GenEO contributions u at the copies of e

@@ -139,6 +139,11 @@ def test_sweep_is_grid_independent_and_reproducible():
         G.apply_coarse(v, y[1])
         G.apply_preconditioner(v, y[2])
         outs[grid] = [t.cpu().numpy() for t in y]
+        # repeated applications (the few-CTA grid streams many tasks per CTA
+        # through the descriptor / tile rings: the race-prone regime)
+        for _ in range(10):
+            G.apply_preconditioner(v, y[0])
+            assert np.array_equal(y[0].cpu().numpy(), outs[grid][2])
         G.close()
     for name, a, b in zip(("local", "coarse", "preconditioner"), outs["0"], outs["5"]):
         assert np.array_equal(a, b), f"{name}: max rel diff {np.abs(a - b).max() / np.abs(a).max():.3e}"
