@@ -180,12 +180,18 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     X.voff = (int)(lo - X.vlo2);
     X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
   };
+  // the fixed cost of one M task in byte equivalents (~1.5 us of one CTA's
+  // streaming rate: task start, partial-sum store, atomic)
+  constexpr int64_t kTaskCostBytes = 24 * 1024;
   struct Cand {
     int64_t bytes;
     dev::MTaskDesc d;
     std::vector<int> tiles;
   };
-  // persistent grid (needed to size the 2-D tile groups)
+  // persistent grid (needed to size the 2-D tile groups; plan_grid, the full
+  // resident grid, fixes the grouping and hence the summation order even when
+  // MDD_SWEEP_GRID runs fewer CTAs)
+  int plan_grid = 0;
   const int smem = dev::kSweepSmemDoubles * (int)sizeof(double);
   CUDA_CHECK(cudaFuncSetAttribute(dev::k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   {
@@ -194,7 +200,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev_id));
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_sweep, dev::kSweepThreads, smem));
     MDD_REQUIRE(per_sm > 0, 5, "sweep kernel cannot be resident");
-    sweep_grid = nsm * per_sm;
+    sweep_grid = plan_grid = nsm * per_sm;
     if (const char* ev = getenv("MDD_SWEEP_GRID")) {  // debug: fewer persistent CTAs
       const int gr = atoi(ev);
       if (gr > 0 && gr < sweep_grid) sweep_grid = gr;
@@ -205,14 +211,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     std::vector<int>& lev = dir == 0 ? lev_f : lev_b;
     for (int l = 0; l < fp.nlevels; ++l) {
       lev[l] = (int)out.size();
+     // the level's tasks with 2-D groups of kGroup tiles
+     auto build_level = [&](const int kGroup) {
       std::vector<Cand> lt;
-      // 2-D tiles per task: fewer, larger tasks only while they still cover the
-      // grid twice over (a level with few tiles is latency-bound)
-      int64_t t2d = 0;
-      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k)
-        if (mode[fp.level_sn[k]] == 2) t2d += (int64_t)(dir == 0 ? ft : bt)[fp.level_sn[k]].size();
-      (void)t2d;
-      const int kGroup = 4;
       for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
         const int g = fp.level_sn[k];
         const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
@@ -297,6 +298,25 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         MDD_REQUIRE(c.d.vbytes <= (int)((dev::kVecMax + 2) * sizeof(double)), 5,
                     "sweep task vector exceeds its shared-memory slot");
       std::stable_sort(lt.begin(), lt.end(), [](const Cand& x, const Cand& y) { return x.bytes > y.bytes; });
+      return lt;
+     };
+      // group size of the 2-D tiles: the one whose snake dealing gives the
+      // smallest per-CTA load (bytes + a fixed cost per task: its start, the
+      // partial sums and the atomic), larger groups on ties.  A phase ends with
+      // its slowest CTA, so on the upper levels (few tiles) smaller groups win.
+      std::vector<Cand> lt;
+      int64_t best = INT64_MAX;
+      for (int kGroup : {4, 2, 1}) {
+        std::vector<Cand> c = build_level(kGroup);
+        std::vector<int64_t> load(plan_grid, 0);
+        for (size_t i = 0; i < c.size(); ++i) {
+          const int64_t r = (int64_t)i / plan_grid, q = (int64_t)i % plan_grid;
+          load[(r & 1) ? plan_grid - 1 - q : q] += c[i].bytes + kTaskCostBytes;
+        }
+        const int64_t mk = *std::max_element(load.begin(), load.end());
+        if (mk < best) { best = mk; lt.swap(c); }
+        if (getenv("MDD_FIXED_GROUP")) break;  // debug: always groups of 4
+      }
       for (auto& c : lt) {
         dev::MTaskDesc X = c.d;
         X.k0 = (int)td.size();
