@@ -55,6 +55,7 @@ class MaxwellDD:
 
     def __init__(self, w, coarse="snk", variant="as2", device=0, geneo=True):
         self.w = w
+        self.variant = variant
         d, keep = _desc(w, coarse, variant, device, geneo)
         h = C.c_void_p()
         L.check(L.lib().mdd_setup(C.byref(d), C.byref(h)))
@@ -163,8 +164,12 @@ class MaxwellDD:
                   + 8 * i["n0"] + 16 * n) if i["n0"] else 0
         vec = 8 * n * 4
         precond = local + 2 * coarse + 2 * spmv + vec
+        # the PCG loop's preconditioner: with the coarse start (reading R13) one
+        # coarse correction and one A product, w + Q (r - A w)
+        loop = local + coarse + spmv + 8 * n * 5 if getattr(self, "variant", "as2") == "as2_coarse_start" \
+            else precond
         return {"spmv": spmv, "local": local, "coarse": coarse, "precond": precond,
-                "iteration": precond + spmv + 8 * n * 7}
+                "precond_in_loop": loop, "iteration": loop + spmv + 8 * n * 7}
 
     def apply_preconditioner(self, r, z):
         L.check(L.lib().mdd_apply_preconditioner(self._h, _ptr(r), _ptr(z)))
