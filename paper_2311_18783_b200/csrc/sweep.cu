@@ -68,10 +68,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
 
 // grid-wide barrier over co-resident CTAs (cumulative counter, no reset)
 __device__ void grid_barrier(unsigned long long* ctl, unsigned long long target) {
+  // bar.sync orders the CTA's writes before thread 0's release add; thread 0's
+  // acquire load and the second bar.sync order every later read after the other
+  // CTAs' writes (release/acquire at gpu scope, no full fence)
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&ctl[SW_BAR], 1ull);
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&ctl[SW_BAR]) : "memory");
     if (ld_acquire(&ctl[SW_BAR]) < target) {
       const unsigned long long t0 = globaltimer();
       for (int it = 0;; ++it) {
@@ -86,7 +88,6 @@ __device__ void grid_barrier(unsigned long long* ctl, unsigned long long target)
         }
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -450,7 +451,6 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             // last group of the row / column block to combine
             unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
             unsigned long long old;
-            __threadfence();
             asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(c) : "memory");
             s_flag = old + 1 == cur * (unsigned long long)D.ntl;
           }
