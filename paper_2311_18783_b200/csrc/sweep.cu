@@ -77,7 +77,7 @@ __device__ void grid_barrier(unsigned long long* ctl, unsigned long long target)
     if (ld_acquire(&ctl[SW_BAR]) < target) {
       const unsigned long long t0 = globaltimer();
       for (int it = 0;; ++it) {
-        __nanosleep(64);
+        __nanosleep(it < 64 ? 16 : 64);
         if (ld_acquire(&ctl[SW_BAR]) >= target) break;
         if ((it & 255) == 255) {
           if (*(volatile unsigned long long*)&ctl[SW_ABORT]) break;
