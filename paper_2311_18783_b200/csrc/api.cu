@@ -834,7 +834,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     const char* place = getenv("MDD_GENEO_PLACE");
     if (!(place && std::string(place) == "last")) esys.box = ebox.data();
     std::vector<SymSystem> sys{esys};
-    build_factor_plan(H->crs.fp, sys, env_int("MDD_ND_LEAF", 64));
+    build_factor_plan(H->crs.fp, sys, env_int("MDD_ND_LEAF_COARSE", 32));
     H->crs.name = "coarse";
     H->crs.upload();
     H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);

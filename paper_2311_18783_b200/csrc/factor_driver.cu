@@ -182,7 +182,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   };
   // the fixed cost of one M task in byte equivalents (~1.5 us of one CTA's
   // streaming rate: task start, partial-sum store, atomic)
-  constexpr int64_t kTaskCostBytes = 24 * 1024;
+  const int64_t kTaskCostBytes = getenv("MDD_TASK_COST") ? atoll(getenv("MDD_TASK_COST")) : 24 * 1024;
   struct Cand {
     int64_t bytes;
     dev::MTaskDesc d;
@@ -306,7 +306,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       // its slowest CTA, so on the upper levels (few tiles) smaller groups win.
       std::vector<Cand> lt;
       int64_t best = INT64_MAX;
+      const int only_group = getenv("MDD_GROUP") ? atoi(getenv("MDD_GROUP")) : 0;  // debug
       for (int kGroup : {4, 2, 1}) {
+        if (only_group && kGroup != only_group) continue;
         std::vector<Cand> c = build_level(kGroup);
         std::vector<int64_t> load(plan_grid, 0);
         for (size_t i = 0; i < c.size(); ++i) {
