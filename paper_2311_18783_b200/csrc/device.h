@@ -82,7 +82,7 @@ struct DevFactor {
   DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc;
   DBuf<int32_t> gsrc;
   DBuf<double> Lt, fpart, bpart, vb;
-  DBuf<unsigned long long> rb_cnt, cb_cnt, ticket, ctl, trace;
+  DBuf<unsigned long long> rb_cnt, cb_cnt, ctl, trace;
   int nphases = 0, nphases_noprolong = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
   int64_t lt_size = 0;
   const int64_t* pro_ptr = nullptr;

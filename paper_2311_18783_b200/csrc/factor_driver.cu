@@ -179,6 +179,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     X.vlo2 = lo & ~1LL;
     X.voff = (int)(lo - X.vlo2);
     X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
+    X.vn = (int)(hi - lo);
   };
   // the fixed cost of one M task in byte equivalents (~1.5 us of one CTA's
   // streaming rate: task start, partial-sum store, atomic)
@@ -329,15 +330,23 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     }
     lev[fp.nlevels] = (int)out.size();
   }
+  // levels with few tasks per CTA gather their task vectors inside the tasks (no
+  // flat G phase and no grid barrier before them); the leaf levels keep the
+  // flat gather (many rows, many tasks per CTA).  Same sums in the same order.
+  const int fuse_tasks = getenv("MDD_FUSE_TASKS") ? atoi(getenv("MDD_FUSE_TASKS")) : 2;
+  auto fused = [&](const std::vector<int>& lev, int l) {
+    return lev[l + 1] - lev[l] <= fuse_tasks * plan_grid;
+  };
   std::vector<int4> ph;
-  int nm = 0;
   for (int l = 0; l < fp.nlevels; ++l) {
-    ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
-    ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], nm++));
+    const bool fz = fused(lev_f, l);
+    if (!fz) ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
+    ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], fz ? 1 : 0));
   }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
-    ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
-    ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], nm++));
+    const bool fz = fused(lev_b, l);
+    if (!fz) ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
+    ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], fz ? 1 : 0));
   }
   nphases_noprolong = (int)ph.size();
   if (prolong_n > 0) {
@@ -367,7 +376,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   bpart.alloc(std::max<int64_t>(nbp, 1));
   rb_cnt.alloc(std::max(nrbc, 1));
   cb_cnt.alloc(std::max(ncbc, 1));
-  ticket.alloc(std::max(nm, 1));
   ctl.alloc(dev::SW_COUNT);
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
@@ -398,7 +406,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
 }
 
 void DevFactor::reset_counters(cudaStream_t s) {
-  for (DBuf<unsigned long long>* c : {&rb_cnt, &cb_cnt, &ticket})
+  for (DBuf<unsigned long long>* c : {&rb_cnt, &cb_cnt})
     CUDA_CHECK(cudaMemsetAsync(c->p, 0, c->n * sizeof(unsigned long long), s));
   std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
   c0[dev::SW_T0] = ~0ull;
@@ -412,7 +420,6 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.dinv = dinv.p;
   S.phases = phases.p;
   S.nphases = nphases;
-  S.ticket = ticket.p;
   S.mtf = mt_f.p;
   S.mtb = mt_b.p;
   S.tdesc = tdesc.p;

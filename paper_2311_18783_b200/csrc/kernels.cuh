@@ -116,6 +116,7 @@ struct __align__(16) MTaskDesc {
   int ntl;          // big: tiles combined by the last arriver
   int voff;         // offset of the vector inside its shared-memory buffer
   int vbytes;       // bytes of the vector bulk copy
+  int vn;           // rows of the task vector (vb rows [vlo2 + voff, + vn))
 };
 
 struct SweepDev {
@@ -123,10 +124,10 @@ struct SweepDev {
   const double* dinv;
   const MTaskDesc* mtf;          // M tasks, forward / backward descriptors
   const MTaskDesc* mtb;
-  // phases {kind, a, b, ticket slot}: G: rows [a, b) of vb; M: mtask [a, b); PR
+  // phases {kind, a, b, w}: G: rows [a, b) of vb; M: mtask [a, b), w = 1 when the
+  // level's gather is fused into its tasks (no G phase before it); PR
   const int4* phases;
   int nphases;
-  unsigned long long* ticket;    // (unused: M tasks are dealt statically)
   const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
   const int64_t* tile_off;       // into Lt

@@ -23,12 +23,15 @@
 //     row -> contributions list, so no scatter and no atomics)  |  M_f (tiles)
 //   for each level, root first:     G_b  (w = [D z_c ; -x_off])  |  M_b (tiles)
 //   prolongation.
-// Within M phases CTAs take tasks from an atomic ticket (largest first).  A task
-// is either a small supernode (all its column tiles, accumulated in shared
-// memory by one CTA) or one RB x CB tile of a big supernode, whose partial sums
-// the last tile to arrive combines in a fixed order -- every reduction is
-// bit-reproducible.  Counters are cumulative across launches (epoch); a barrier
-// wait that exceeds kSpinTimeoutNs raises an abort flag reported by the host.
+// Levels with few tasks per CTA skip their G phase: each task gathers its own
+// vector rows (same sums, same order).  Within M phases the tasks, sorted
+// largest first, are dealt to the CTAs in snake order (no atomics).  A task is a
+// small supernode (all its packed column tiles, accumulated in shared memory by
+// one CTA), a strip of a wide supernode, or a group of 1-4 RB x CB tiles of a big
+// supernode whose partial sums the last group to arrive combines in a fixed
+// order -- every reduction is bit-reproducible and independent of the grid
+// size.  Counters are cumulative across launches (epoch); a barrier wait that
+// exceeds kSpinTimeoutNs raises an abort flag reported by the host.
 #include "kernels.cuh"
 
 namespace mdd {
@@ -64,6 +67,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       "}\n" ::"r"(smem_u32(m)),
       "r"(parity)
       : "memory");
+}
+
+// one row of the forward task vector: t = [b_c ; 0] + children's updates
+__device__ __forceinline__ double gather_t(const SweepDev& S, long long q) {
+  const int src = S.gsrc[q];
+  double v = src >= 0 ? __ldg(S.b + src) : 0.0;
+  for (i64 k = S.cptr[q]; k < S.cptr[q + 1]; ++k) v += __ldcg(S.upd + S.cidx[k]);
+  return v;
+}
+// one row of the backward task vector: w = [D z_c ; -x_off]
+__device__ __forceinline__ double gather_w(const SweepDev& S, long long q) {
+  const i64 w = S.wsrc[q];
+  return w >= 0 ? __ldcg(S.xf + w) / __ldg(S.dinv + w) : -__ldcg(S.xb + (-w - 1));
 }
 
 // grid-wide barrier over co-resident CTAs (cumulative counter, no reset)
@@ -253,18 +269,10 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
     if (kind == PH_GF) {
       // t = [b_c ; 0] + children's updates, one row per thread
-      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) {
-        const int src = S.gsrc[q];
-        double v = src >= 0 ? __ldg(S.b + src) : 0.0;
-        for (i64 k = S.cptr[q]; k < S.cptr[q + 1]; ++k) v += __ldcg(S.upd + S.cidx[k]);
-        S.vb[q] = v;
-      }
+      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_t(S, q);
     } else if (kind == PH_GB) {
       // w = [D z_c ; -x_off]
-      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) {
-        const i64 w = S.wsrc[q];
-        S.vb[q] = w >= 0 ? __ldcg(S.xf + w) / __ldg(S.dinv + w) : -__ldcg(S.xb + (-w - 1));
-      }
+      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_w(S, q);
     } else if (kind == PH_PR) {
       for (size_t e = gtid; e < (size_t)S.n_out; e += gthreads) {
         double s = 0.0;
@@ -276,6 +284,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       // sorted largest first and dealt to the CTAs in snake order (no atomics);
       // every per-task quantity comes from one packed descriptor.
       const bool fwd = kind == PH_MF;
+      const bool fused = PH.w != 0;  // task vectors gathered by the task itself
       const MTaskDesc* const MT = (fwd ? S.mtf : S.mtb) + PH.y;
       const int ntk = PH.z - PH.y;
       const int b = blockIdx.x, G = gridDim.x;
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         }
         const MTaskDesc& Dp = s_desc[pi % kDescRing];
         const bool first = pk == Dp.k0;
-        prefetch(pk, ps % kStages, Dp.vlo2, first ? Dp.vbytes : 0, pi % kVecSlots);
+        prefetch(pk, ps % kStages, Dp.vlo2, first && !fused ? Dp.vbytes : 0, pi % kVecSlots);
         ++ps;
         ++pk;
       };
@@ -361,7 +370,14 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           }
         }
         const MTaskDesc D = s_desc[i % kDescRing];
-        const double* const vv = vbase + (i % kVecSlots) * (kVecMax + 2) + D.voff;  // this task's vector
+        double* const vvw = vbase + (i % kVecSlots) * (kVecMax + 2) + D.voff;
+        const double* const vv = vvw;  // this task's vector
+        if (fused) {
+          // the gathers overlap the task's first tile, already in flight
+          const long long lo = D.vlo2 + D.voff;
+          for (int q = tid; q < D.vn; q += kSweepThreads) vvw[q] = fwd ? gather_t(S, lo + q) : gather_w(S, lo + q);
+          __syncthreads();
+        }
         int buf = 0;
         // wait for the next tile of the stream (its ring slot becomes `buf`)
         auto next_tile_and_wait = [&](int) {
@@ -481,7 +497,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
                 if (fwd) {
                   const int r = D.rb * D.RB + o;
                   if (r < D.nc) S.xf[D.col0 + r] = sum;
-                  else S.upd[D.uptr + (r - D.nc)] = __ldcg(S.vb + D.vo + r) - sum;
+                  else S.upd[D.uptr + (r - D.nc)] = (fused ? gather_t(S, D.vo + r) : __ldcg(S.vb + D.vo + r)) - sum;
                 } else {
                   S.xb[D.col0 + D.cb * D.CB + o] = sum;
                 }
