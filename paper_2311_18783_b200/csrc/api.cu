@@ -264,8 +264,8 @@ struct mdd_solver {
   // A x with 8 lanes per row on an SM-sized grid (nparts blocks: the fused dot's
   // partials are reduced by one small kernel)
   void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
-            double* out, const double* dotw = nullptr, double* part_ = nullptr) {
-    dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, out, dotw, part_, state.p);
+            double* out, const double* dotw = nullptr, double* part_ = nullptr, const double* sub = nullptr) {
+    dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
     launches += 1;
   }
   void applyA(const double* in, double* out) {
@@ -281,9 +281,11 @@ struct mdd_solver {
   }
   // y = Z E^{-1} Z^T v: Z_g^T v (CSR) and Z_e^T v (tall-skinny over the GenEO blocks),
   // the sweep on E, then Z_g xc + prolongation of the GenEO blocks' W_i xc_i
-  void apply_coarse(const double* v, double* y) {
+  // (addw, dotw: y = addw + Q v and dotw . y partials into part, fused into the
+  // last kernel; used by the PCG loop's coarse-start form)
+  void apply_coarse(const double* v, double* y, const double* addw = nullptr, const double* dotw = nullptr) {
     prof_begin(MDD_PROF_COARSE);
-    dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, xc.p,
+    dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, nullptr, xc.p,
                                               nullptr, nullptr, state.p);
     if (nbzt) {
       dev::k_geneo_zt<<<nbzt, 256, 0, stream>>>(W_bzt.p, W_off.p, W_poff.p, W_n.p, W_gc0.p, W_gpos.p, W_val.p,
@@ -296,7 +298,8 @@ struct mdd_solver {
       dev::k_geneo_z<<<nbz, 256, 0, stream>>>(W_bz.p, W_off.p, W_poff.p, W_n.p, W_k.p, W_gc0.p, W_gpos.p,
                                               W_val.p, crs.xb.p, u_loc.p, state.p);
     dev::k_z_apply<<<nparts, 256, 0, stream>>>(n, Zg_ptr.p, Zg_idx.p, Zg_val.p, crs.xb.p, pro_ptr.p, pro_pos.p,
-                                              nbz ? u_loc.p : nullptr, y, state.p);
+                                              nbz ? u_loc.p : nullptr, addw, y, dotw, dotw ? part.p : nullptr,
+                                              state.p);
     prof_end();
     launches += 3 + (nbzt ? 2 : 0) + (nbz ? 1 : 0);
   }
@@ -332,11 +335,16 @@ struct mdd_solver {
       return;
     }
     apply_local(rr, t4.p);                                         // w = M_AS r
-    applyA(t4.p, t2.p);                                            // A w
-    dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, rr, -1.0, t2.p, t3.p, state.p);  // r - A w
-    apply_coarse(t3.p, t1.p);                                      // Q (r - A w)
-    dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, t4.p, 1.0, t1.p, zz, state.p);
-    launches += 2;
+    spmv(A_ptr.p, A_idx.p, A_val.p, n, t4.p, t3.p, nullptr, nullptr, rr);  // r - A w
+    apply_coarse(t3.p, zz, t4.p, rr);   // z = w + Q (r - A w), with the r . z partials
+  }
+  // r . z after apply_prec_loop: the coarse-start form left its partials in part
+  void dot_rz(int slot, int op) {
+    if (!coarse_start()) {
+      dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, z.p, part.p, state.p);
+      launches += 1;
+    }
+    reduce_step(slot, op);
   }
   void check_aborts() {
     loc.check_abort(stream);
@@ -347,22 +355,23 @@ struct mdd_solver {
     dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
     launches += 2;
   }
-  void scalar(int op) {
-    dev::k_scalar_step<<<1, 1, 0, stream>>>(op, S.p, state.p);
+  // S[slot] = reduced partials, then the CG scalar step `op`, in one launch
+  void reduce_step(int slot, int op) {
+    dev::k_reduce_step<<<1, 256, 0, stream>>>(nparts, part.p, S.p, slot, op, state.p);
     launches += 1;
   }
   // ---------------------------------------------------------------- PCG
   // prologue (x = 0 and r = f staged by the host): ||f||, z = M r, p = z, rz
   void enqueue_prologue() {
-    dot(r.p, r.p, dev::S_RR);
-    scalar(3);
+    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, r.p, part.p, state.p);
+    launches += 1;
+    reduce_step(dev::S_RR, 3);
     if (coarse_start()) {
       // x0 = Q f, r0 = f - A x0 (the staged x is 0; reading R13)
       apply_coarse(r.p, x.p);
-      applyA(x.p, t2.p);
-      dev::k_axpby<<<nblk(n, 256), 256, 0, stream>>>(n, 1.0, r.p, -1.0, t2.p, t3.p, state.p);
+      spmv(A_ptr.p, A_idx.p, A_val.p, n, x.p, t3.p, nullptr, nullptr, r.p);
       dev::k_copy<<<nblk(n, 256), 256, 0, stream>>>(n, t3.p, r.p, state.p);
-      launches += 2;
+      launches += 1;
     }
     apply_prec_loop(r.p, z.p);
     dev::k_copy<<<nblk(n, 256), 256, 0, stream>>>(n, z.p, p.p, state.p);
@@ -375,18 +384,14 @@ struct mdd_solver {
     if (mark) mark(2);
     spmv(A_ptr.p, A_idx.p, A_val.p, n, p.p, q.p, p.p, part.p);
     if (mark) mark(3);
-    dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + dev::S_PQ, state.p);
-    launches += 1;
-    scalar(0);
+    reduce_step(dev::S_PQ, 0);
     dev::k_update_xr<<<nparts, 256, 0, stream>>>(n, x.p, r.p, p.p, q.p, S.p, part.p, state.p);
-    dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + dev::S_RR, state.p);
-    launches += 2;
-    scalar(1);
+    launches += 1;
+    reduce_step(dev::S_RR, 1);
     if (mark) mark(4);
     apply_prec_loop(r.p, z.p);
     if (mark) mark(5);
-    dot(r.p, z.p, dev::S_RZNEW);
-    scalar(2);
+    dot_rz(dev::S_RZNEW, 2);
     dev::k_update_p<<<nparts, 256, 0, stream>>>(n, p.p, z.p, S.p, state.p);
     launches += 1;
     if (mark) mark(6);

@@ -446,7 +446,8 @@ template <int TPR>
 __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict__ ptr,
                                                 const int32_t* __restrict__ idx,
                                                 const double* __restrict__ val,
-                                                const double* __restrict__ x, double* __restrict__ y,
+                                                const double* __restrict__ x,
+                                                const double* __restrict__ sub, double* __restrict__ y,
                                                 const double* __restrict__ dotw, double* __restrict__ part,
                                                 const int* __restrict__ stop) {
   if (STOPPED) return;
@@ -472,6 +473,7 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
 #pragma unroll
     for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, TPR);
     if (active && lane == 0) {
+      if (sub) s = sub[row] - s;
       y[row] = s;
       if (dotw) dsum += dotw[row] * s;
     }
@@ -481,9 +483,10 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
 #define MDD_SPMV_G(NAME, TPR)                                                                      \
   __global__ void __launch_bounds__(256)                                                           \
       NAME(int nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,          \
-           const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y, \
-           const double* __restrict__ dotw, double* __restrict__ part, const int* __restrict__ stop) { \
-    spmv_g_body<TPR>(nrows, ptr, idx, val, x, y, dotw, part, stop);                               \
+           const double* __restrict__ val, const double* __restrict__ x,                          \
+           const double* __restrict__ sub, double* __restrict__ y, const double* __restrict__ dotw, \
+           double* __restrict__ part, const int* __restrict__ stop) {                              \
+    spmv_g_body<TPR>(nrows, ptr, idx, val, x, sub, y, dotw, part, stop);                          \
   }
 MDD_SPMV_G(k_spmv8, 8)
 MDD_SPMV_G(k_spmv16, 16)
@@ -601,15 +604,21 @@ __global__ void __launch_bounds__(256) k_z_apply(int n, const int64_t* __restric
                                                  const int32_t* __restrict__ idx, const double* __restrict__ val,
                                                  const double* __restrict__ xc, const int64_t* __restrict__ pptr,
                                                  const int32_t* __restrict__ ppos, const double* __restrict__ u,
-                                                 double* __restrict__ out, const int* __restrict__ stop) {
+                                                 const double* __restrict__ addw, double* __restrict__ out,
+                                                 const double* __restrict__ dotw, double* __restrict__ part,
+                                                 const int* __restrict__ stop) {
   if (STOPPED) return;
+  double d = 0.0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int64_t k = ptr[e]; k < ptr[e + 1]; ++k) s += val[k] * xc[idx[k]];
     if (u)
       for (int64_t k = pptr[e]; k < pptr[e + 1]; ++k) s += u[ppos[k]];
+    if (addw) s = addw[e] + s;
     out[e] = s;
+    if (dotw) d += dotw[e] * s;  // the same per-thread order as k_dot_part
   }
+  if (part) block_sum_store(d, part);
 }
 
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
@@ -634,8 +643,7 @@ __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __
 
 // scalar recurrences of PCG (single thread).  state[ST_STOP] makes every later
 // kernel of the iteration a no-op; state[ST_ITERS] counts iterations on the device
-__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state) {
-  if (state[ST_STOP]) return;
+__device__ void scalar_op(int op, double* __restrict__ S, int* __restrict__ state) {
   switch (op) {
     case 0:  // after q = A p:  alpha = rz / pq
       if (!(S[S_PQ] > 0.0)) { state[ST_BREAKDOWN] = 1; state[ST_STOP] = 1; return; }
@@ -659,6 +667,27 @@ __global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ 
       if (!(S[S_NF] > 0.0)) { state[ST_CONVERGED] = 1; state[ST_STOP] = 1; }
       else if (state[ST_MAXIT] <= 0) state[ST_STOP] = 1;
       break;
+  }
+}
+
+__global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state) {
+  if (state[ST_STOP]) return;
+  scalar_op(op, S, state);
+}
+
+// S[slot] = sum of the block partials (fixed order, as k_reduce), then scalar op
+// `op` on one thread: one launch instead of two per CG scalar
+__global__ void k_reduce_step(int nparts, const double* __restrict__ part, double* __restrict__ S, int slot,
+                              int op, int* __restrict__ state) {
+  if (state[ST_STOP]) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+  __shared__ double tmp[1];
+  block_sum_store(s, tmp);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S[slot] = tmp[0];
+    scalar_op(op, S, state);
   }
 }
 

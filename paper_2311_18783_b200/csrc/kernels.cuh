@@ -191,12 +191,14 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
                        const double* __restrict__ val, const double* __restrict__ x,
                        double* __restrict__ y, const double* __restrict__ dotw,
                        double* __restrict__ part, const int* __restrict__ stop);
-// y = M x, 8 / 16 / 32 lanes per row on an SM-sized grid, optional fused dot partials
+// y = M x (or y = sub - M x), 8 / 16 / 32 lanes per row on an SM-sized grid,
+// optional fused dot partials of dotw . y
 #define MDD_SPMV_G_DECL(NAME)                                                                    \
   __global__ void NAME(int nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx, \
                        const double* __restrict__ val, const double* __restrict__ x,                \
-                       double* __restrict__ y, const double* __restrict__ dotw,                     \
-                       double* __restrict__ part, const int* __restrict__ stop);
+                       const double* __restrict__ sub, double* __restrict__ y,                      \
+                       const double* __restrict__ dotw, double* __restrict__ part,                  \
+                       const int* __restrict__ stop);
 MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
 MDD_SPMV_G_DECL(k_spmv32)
@@ -218,12 +220,16 @@ __global__ void k_geneo_z(const int4* __restrict__ blk, const int64_t* __restric
 __global__ void k_z_apply(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                           const double* __restrict__ val, const double* __restrict__ xc,
                           const int64_t* __restrict__ pptr, const int32_t* __restrict__ ppos,
-                          const double* __restrict__ u, double* __restrict__ out, const int* __restrict__ stop);
+                          const double* __restrict__ u, const double* __restrict__ addw,
+                          double* __restrict__ out, const double* __restrict__ dotw,
+                          double* __restrict__ part, const int* __restrict__ stop);
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ part, const int* __restrict__ stop);
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
                          const int* __restrict__ stop);
 __global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state);
+__global__ void k_reduce_step(int nparts, const double* __restrict__ part, double* __restrict__ S, int slot,
+                              int op, int* __restrict__ state);
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ state);
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
                             const double* __restrict__ p, const double* __restrict__ q,
