@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmaxwell_dd.so")
+# MDD_LIB_PATH: an experiment build of the same library (tools/, never the default)
+LIB_PATH = os.environ.get("MDD_LIB_PATH") or os.path.join(HERE, "libmaxwell_dd.so")
 
 MDD_OK, MDD_ERR_CUDA, MDD_ERR_ARG, MDD_ERR_NOTPD, MDD_ERR_NOCONV, MDD_ERR_INTERNAL, MDD_ERR_BREAKDOWN = range(7)
 DIRICHLET = {"outer": 0, "all": 1, "none": 2}

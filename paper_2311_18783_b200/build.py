@@ -7,7 +7,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libmaxwell_dd.so")
+LIB = os.environ.get("MDD_LIB_PATH") or os.path.join(HERE, "libmaxwell_dd.so")
+# experiment builds only (e.g. -DMDD_DEBUG_NOCOMPUTE with MDD_LIB_PATH elsewhere)
+EXTRA = os.environ.get("MDD_NVCC_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
@@ -26,13 +28,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     deps.append(os.path.join(HERE, "..", "include", "maxwell_dd.h"))
     if not force and not _newer(LIB, deps):
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_x" if EXTRA else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
-        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", *ARCH, *EXTRA, "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(HERE, "..", "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):

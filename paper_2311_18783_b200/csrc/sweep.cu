@@ -150,23 +150,105 @@ __device__ __forceinline__ void tile_matvec(const double* T, int R, int C, const
   }
 }
 
-// y_j = sum_i T[j*R + i] w[i] (warp per column, lanes down the rows); fin(j, y_j)
-template <class Fin>
-__device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, const double* w, Fin fin) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < C; j += kWarps) {
-    const double* col = T + j * R;
-    double s0 = 0.0, s1 = 0.0;
-    int i = lane;
-    for (; i + 32 < R; i += 64) {
-      s0 += col[i] * w[i];
-      s1 += col[i + 32] * w[i + 32];
+// Butterfly reduce-scatter of 8 per-lane partial sums (one per column of a group
+// of 8) over the 32 lanes of a warp: 9 shuffles instead of 8 x 5.  Returns, in
+// every lane, the full sum of column (lane >> 2); a fixed order (deterministic).
+__device__ __forceinline__ double warp_reduce8(const double (&p)[8], int lane) {
+  double q[4], r[2];
+  {
+    const bool hi = (lane >> 4) & 1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double keep = hi ? p[k + 4] : p[k], send = hi ? p[k] : p[k + 4];
+      q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    if (i < R) s0 += col[i] * w[i];
-    const double s = warp_sum(s0 + s1);
-    if (lane == 0) fin(j, s);
+  }
+  {
+    const bool hi = (lane >> 3) & 1;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double keep = hi ? q[k + 2] : q[k], send = hi ? q[k] : q[k + 2];
+      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  const bool hi = (lane >> 2) & 1;
+  const double keep = hi ? r[1] : r[0], send = hi ? r[0] : r[1];
+  double s = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// The same for 4 columns: the full sum of column (lane >> 3) in every lane.
+__device__ __forceinline__ double warp_reduce4(const double (&p)[4], int lane) {
+  double q[2];
+  {
+    const bool hi = (lane >> 4) & 1;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double keep = hi ? p[k + 2] : p[k], send = hi ? p[k] : p[k + 2];
+      q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  const bool hi = (lane >> 3) & 1;
+  const double keep = hi ? q[1] : q[0], send = hi ? q[0] : q[1];
+  double s = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// y_j = sum_i T[j*R + i] w[i] for j < C (T col-major in smem).  Work unit: a
+// warp x (a group of 8 columns, a slice of the rows); lanes run down the rows
+// with 8 partial sums, then warp_reduce8; several row slices (when the columns
+// are too few to occupy the warps) are added in order through `red`.  fin(j, y_j)
+// once per column.  Callers __syncthreads after.
+template <int W, class Fin>
+__device__ __forceinline__ void tile_matvec_t_w(const double* T, int R, int C, const double* w, double* red,
+                                                Fin fin) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = (C + W - 1) / W;
+  const int nsl = G >= kWarps ? 1 : kWarps / G;
+  constexpr int kSh = W == 8 ? 2 : 3;  // lane >> kSh = the column a lane ends with
+  for (int jb = warp; jb < G * nsl; jb += kWarps) {
+    const int g = jb % G, sl = jb / G;
+    const int r0 = (sl * R) / nsl, r1 = ((sl + 1) * R) / nsl;
+    double p[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) p[k] = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) {
+      const double wi = w[i];
+#pragma unroll
+      for (int k = 0; k < W; ++k)
+        if (g * W + k < C) p[k] += T[(g * W + k) * R + i] * wi;
+    }
+    double v;
+    if constexpr (W == 8) v = warp_reduce8(p, lane);
+    else v = warp_reduce4(p, lane);
+    const int j = g * W + (lane >> kSh);
+    if ((lane & ((1 << kSh) - 1)) == 0 && j < C) {
+      if (nsl == 1) fin(j, v);
+      else red[sl * C + j] = v;
+    }
+  }
+  if (nsl > 1) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < C; j += kSweepThreads) {
+      double y = 0.0;
+      for (int q = 0; q < nsl; ++q) y += red[q * C + j];
+      fin(j, y);
+    }
   }
 }
+// groups of 8 columns for wide tiles (2-D: 64 columns), of 4 for narrow ones
+template <class Fin>
+__device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, const double* w, double* red,
+                                              Fin fin) {
+  if (C >= 48) tile_matvec_t_w<8>(T, R, C, w, red, fin);
+  else tile_matvec_t_w<4>(T, R, C, w, red, fin);
+}
+
 // Packed lower-trapezoidal column tile of a small supernode: columns c0 .. c0+C-1
 // of an nr-row panel, column jj holding rows c0+jj .. nr-1 (the zeros above the
 // diagonal are not stored), column offsets coff(jj) = jj (nr - c0) - jj (jj - 1) / 2.
@@ -216,9 +298,11 @@ __device__ __forceinline__ void tile_matvec_packed(const double* T, int nr, int 
 }
 
 // Backward on a packed tile: x_jj = sum_{i >= c0+jj} T(i, c0+jj) w[i]; fin(jj, x)
+#ifdef MDD_PACKED_T_WARP
+// experiment: one warp per column
 template <class Fin>
 __device__ __forceinline__ void tile_matvec_t_packed(const double* T, int nr, int c0, int C, const double* w,
-                                                     Fin fin) {
+                                                     double*, Fin fin) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = nr - c0;
   for (int jj = warp; jj < C; jj += kWarps) {
@@ -236,6 +320,45 @@ __device__ __forceinline__ void tile_matvec_t_packed(const double* T, int nr, in
     if (lane == 0) fin(jj, s);
   }
 }
+#else
+template <class Fin>
+__device__ __forceinline__ void tile_matvec_t_packed(const double* T, int nr, int c0, int C, const double* w,
+                                                     double* red, Fin fin) {
+  // groups of 4 columns (a small tile has few columns: more warps busy)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = nr - c0;
+  const int G = (C + 3) >> 2;
+  const int nsl = G >= kWarps ? 1 : kWarps / G;
+  for (int jb = warp; jb < G * nsl; jb += kWarps) {
+    const int g = jb % G, sl = jb / G;
+    const int len0 = R - g * 4;  // rows of the group's first (longest) column
+    const int r0 = (sl * len0) / nsl, r1 = ((sl + 1) * len0) / nsl;
+    double p[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = r0 + lane; i < r1; i += 32) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int jj = g * 4 + k;
+        // column jj holds rows c0+jj .. nr-1 at coff(jj) = jj R - jj (jj - 1) / 2
+        if (jj < C && i < R - jj) p[k] += T[jj * R - (jj * (jj - 1)) / 2 + i] * w[c0 + jj + i];
+      }
+    }
+    const double v = warp_reduce4(p, lane);
+    const int jj = g * 4 + (lane >> 3);
+    if ((lane & 7) == 0 && jj < C) {
+      if (nsl == 1) fin(jj, v);
+      else red[sl * C + jj] = v;
+    }
+  }
+  if (nsl > 1) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < C; j += kSweepThreads) {
+      double y = 0.0;
+      for (int q = 0; q < nsl; ++q) y += red[q * C + j];
+      fin(j, y);
+    }
+  }
+}
+#endif
 }  // namespace
 
 __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
@@ -390,6 +513,15 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           if (tid == 0) issue_next();
           ++cs;
         };
+#ifdef MDD_DEBUG_NOCOMPUTE
+        if (true) {  // timing experiment: stream the tiles, skip the arithmetic
+          for (int kk = D.k0; kk < D.k1; ++kk) {
+            next_tile_and_wait(kk);
+            __syncthreads();
+            tile_done();
+          }
+        } else
+#endif
         if (D.big == 2) {
           // ---------------- strip of a wide supernode (nr <= kVecMax): fwd = rows
           // [r0, r0+rows) x all columns, bwd = all rows x columns [c0, c0+cols);
@@ -405,7 +537,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             });
           } else {
             double* const xb = S.xb + D.col0 + D.cb;
-            tile_matvec_t(T, D.nr, D.cols, vv, [&](int j, double y) { xb[j] = y; });
+            tile_matvec_t(T, D.nr, D.cols, vv, red, [&](int j, double y) { xb[j] = y; });
           }
           __syncthreads();
           tile_done();
@@ -424,7 +556,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
                 tile_matvec_packed(T, D.nr, c0, cols, vv + c0, red, [&](int r, double y) { vec2[r] += y; });
             } else {
               double* const xb = S.xb + D.col0 + c0;
-              tile_matvec_t_packed(T, D.nr, c0, cols, vv, [&](int j, double y) { xb[j] = y; });
+              tile_matvec_t_packed(T, D.nr, c0, cols, vv, red, [&](int j, double y) { xb[j] = y; });
             }
             __syncthreads();
             tile_done();
@@ -450,8 +582,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
               else tile_matvec(T, D.rows, cols, vv + j * D.CB, red, [&](int r, double y) { vec2[r] += y; });
             } else {
               const int rows = min(D.RB, D.nr - (D.rb + j) * D.RB);
-              if (j == 0) tile_matvec_t(T, rows, D.cols, vv, [&](int c, double y) { vec2[c] = y; });
-              else tile_matvec_t(T, rows, D.cols, vv + j * D.RB, [&](int c, double y) { vec2[c] += y; });
+              if (j == 0) tile_matvec_t(T, rows, D.cols, vv, red, [&](int c, double y) { vec2[c] = y; });
+              else tile_matvec_t(T, rows, D.cols, vv + j * D.RB, red, [&](int c, double y) { vec2[c] += y; });
             }
             __syncthreads();
             tile_done();
