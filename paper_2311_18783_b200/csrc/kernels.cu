@@ -567,7 +567,8 @@ __global__ void k_geneo_zt2(int ncols, const int* __restrict__ cblk, const int* 
   y[gpos[c]] = t;
 }
 
-// u[off_i + p] = sum_k W_i[p + k n_i] xc[gpos[gcol0_i + k]]  (rows of subdomain i)
+// u[off_i + p] = sum_k W_i[p + k n_i] xc[gpos[gcol0_i + k]]  (rows of subdomain i);
+// the block's k_i coarse values are staged in shared memory (64 at a time)
 __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                                                  const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                                                  const int* __restrict__ kcnt, const int* __restrict__ gcol0,
@@ -575,28 +576,34 @@ __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, c
                                                  const double* __restrict__ xc, double* __restrict__ u,
                                                  const int* __restrict__ stop) {
   if (STOPPED) return;
+  __shared__ double xs[64];
   const int4 b = blk[blockIdx.x];  // {subdomain, first row, -, -}
   const int i = b.x;
   const int ni = nsz[i], ki = kcnt[i];
   const int p = b.y + threadIdx.x;
-  if (p >= ni) return;
+  const bool act = p < ni;
   const double* Wi = W + woff[i];
   const int32_t* gp = gpos + gcol0[i];
-  // eight independent column streams in flight per thread
+  // eight independent column streams in flight per thread; column k goes to s[k % 8]
   double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  int k = 0;
-  for (; k + 8 <= ki; k += 8) {
-    double w[8], x[8];
+  for (int kb = 0; kb < ki; kb += 64) {
+    const int kn = min(64, ki - kb);
+    __syncthreads();
+    if (threadIdx.x < kn) xs[threadIdx.x] = __ldg(xc + __ldg(gp + kb + threadIdx.x));
+    __syncthreads();
+    if (act) {
+      int k = 0;
+      for (; k + 8 <= kn; k += 8) {
+        double w[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      w[j] = __ldcs(Wi + (int64_t)(k + j) * ni + p);
-      x[j] = __ldg(xc + __ldg(gp + k + j));
+        for (int j = 0; j < 8; ++j) w[j] = __ldcs(Wi + (int64_t)(kb + k + j) * ni + p);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[j] += w[j] * xs[k + j];
+      }
+      for (int j = 0; k < kn; ++k, ++j) s[j] += __ldcs(Wi + (int64_t)(kb + k) * ni + p) * xs[k];
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s[j] += w[j] * x[j];
   }
-  for (int j = 0; k < ki; ++k, ++j) s[j] += __ldcs(Wi + (int64_t)k * ni + p) * __ldg(xc + __ldg(gp + k));
-  u[poff[i] + p] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  if (act) u[poff[i] + p] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 // out[e] = Z_g(e, :) xc + sum of the GenEO contributions u at the copies of e
