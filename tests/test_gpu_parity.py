@@ -51,6 +51,11 @@ CASES = {
     "c1-recipe-8": lambda: workloads.make("c1", n=8, p=2),
     "holes-8": _holes,
     "c2-recipe-12": lambda: workloads.make("c2", n=12, p=2, hole=2),
+    # overlap 2, layered mu^-1 (contrast 1e3), per-element eps
+    "c3-recipe-12": lambda: workloads.make("c3", n=12, p=2),
+    # random 1e4 inclusions; the two-"GPU" weak-scaling box (16x8x8 cubes, 4x2x2 subdomains)
+    "c4-recipe-12": lambda: workloads.make("c4", m=12, q=2),
+    "c4-recipe-x2": lambda: workloads.make("c4", m=8, q=2, ngpu=2),
 }
 _cache = {}
 EPS = np.finfo(float).eps
