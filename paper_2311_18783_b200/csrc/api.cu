@@ -205,6 +205,7 @@ struct mdd_solver {
   DBuf<double> W_part;
   DBuf<int4> W_bzt, W_bz;
   int nbzt = 0, nbz = 0;
+  int spmv_tpr = env_int("MDD_SPMV_TPR", 8);  // lanes per row of the A product (4 / 8 / 16)
   int64_t nnzZg = 0, nnzW = 0;
   int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0, coarse_perturbed = 0;
   std::vector<int64_t> geneo_count;
@@ -265,7 +266,12 @@ struct mdd_solver {
   // partials are reduced by one small kernel)
   void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
             double* out, const double* dotw = nullptr, double* part_ = nullptr, const double* sub = nullptr) {
-    dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+    if (spmv_tpr == 4)
+      dev::k_spmv4<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+    else if (spmv_tpr == 16)
+      dev::k_spmv16<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+    else
+      dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
     launches += 1;
   }
   void applyA(const double* in, double* out) {

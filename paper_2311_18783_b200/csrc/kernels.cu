@@ -488,6 +488,7 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
            double* __restrict__ part, const int* __restrict__ stop) {                              \
     spmv_g_body<TPR>(nrows, ptr, idx, val, x, sub, y, dotw, part, stop);                          \
   }
+MDD_SPMV_G(k_spmv4, 4)
 MDD_SPMV_G(k_spmv8, 8)
 MDD_SPMV_G(k_spmv16, 16)
 MDD_SPMV_G(k_spmv32, 32)

@@ -199,6 +199,7 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
                        const double* __restrict__ sub, double* __restrict__ y,                      \
                        const double* __restrict__ dotw, double* __restrict__ part,                  \
                        const int* __restrict__ stop);
+MDD_SPMV_G_DECL(k_spmv4)
 MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
 MDD_SPMV_G_DECL(k_spmv32)
