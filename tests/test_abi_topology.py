@@ -88,3 +88,21 @@ def test_topology_bit_exact_c1_full_size():
     ptr, dofs = T(w, "sub_ptr"), T(w, "sub_dofs")
     for i, d in enumerate(dec.dofs):
         assert np.array_equal(dofs[ptr[i]:ptr[i + 1]], d)
+
+
+def test_null_handles_and_bad_values_return_errors():
+    """Every entry point rejects null handles / pointers with MDD_ERR_ARG and a
+    message, without touching a device (runs without a GPU)."""
+    import ctypes as C
+    from paper_2311_18783_b200 import _lib as L
+    lib = L.lib()
+    it, rel = C.c_int(0), C.c_double(0.0)
+    assert lib.mdd_solve(None, None, None, 1e-8, 10, C.byref(it), C.byref(rel)) == L.MDD_ERR_ARG
+    assert lib.mdd_last_error()
+    assert lib.mdd_solve_host(None, None, None, 1e-8, 10, C.byref(it), C.byref(rel)) == L.MDD_ERR_ARG
+    for fn in ("mdd_apply_preconditioner", "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse"):
+        assert getattr(lib, fn)(None, None, None) == L.MDD_ERR_ARG, fn
+    assert lib.mdd_set_variant(None, 0) == L.MDD_ERR_ARG
+    assert lib.mdd_set_stream(None, None) == L.MDD_ERR_ARG
+    assert lib.mdd_setup(None, None) == L.MDD_ERR_ARG
+    lib.mdd_destroy(None)   # a no-op

@@ -226,3 +226,19 @@ def test_profiled_eager_solve_matches_graph_solve():
     assert prof["total"][0] > 0 and abs(parts - prof["total"][0]) <= 0.05 * prof["total"][0] + 1e-3
     assert prof["local"][1] in (ite, ite + 1) and prof["coarse"][1] == 2 * prof["local"][1]
     assert min(prof[k][0] for k in ("local", "coarse")) > 0 and prof["prec_other"][0] >= 0
+
+
+@pytest.mark.parametrize("variant", ["as2", "as2_coarse_start"])
+def test_iteration_limit_returns_the_iterate(variant):
+    """maxit reached: MDD_ERR_NOCONV (ok = False), the k-th iterate and its
+    recurrence residual are still returned and match the oracle's PCG stopped
+    at the same k."""
+    w, P, G = pair("c1-recipe-8", variant=variant)
+    f = workloads.rhs(P.n, w.f_seed)
+    k = 5
+    x = torch.empty(P.n, dtype=torch.float64, device="cuda")
+    it, relres, ok = G.solve(dev(f), x, tol=1e-14, maxit=k)
+    xo, ito, hist = P.solve(f, tol=1e-14, maxit=k, x0="coarse" if variant == "as2_coarse_start" else "zero")
+    assert not ok and it == k and ito == k
+    assert abs(relres - hist[-1]) <= 1e-6 * hist[-1]
+    assert rel(host(x), xo) <= tol_for(P, 1e-8, "global")
