@@ -240,5 +240,8 @@ def test_iteration_limit_returns_the_iterate(variant):
     it, relres, ok = G.solve(dev(f), x, tol=1e-14, maxit=k)
     xo, ito, hist = P.solve(f, tol=1e-14, maxit=k, x0="coarse" if variant == "as2_coarse_start" else "zero")
     assert not ok and it == k and ito == k
-    assert abs(relres - hist[-1]) <= 1e-6 * hist[-1]
-    assert rel(host(x), xo) <= tol_for(P, 1e-8, "global")
+    # after k steps the two fp64 trajectories differ at the preconditioner's own
+    # parity level (kappa * eps, reading R9), not at the end-of-solve level
+    t = tol_for(P, 1e-10, "global")
+    assert abs(relres - hist[-1]) <= 4 * t * hist[-1]
+    assert rel(host(x), xo) <= 4 * t

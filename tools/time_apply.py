@@ -15,3 +15,4 @@ def t(fn, reps=20):
     b.record(st); b.synchronize()
     return a.elapsed_time(b) / reps
 print(f"apply_local {t(lambda: G.apply_local(v, y)):.4f} ms  apply_coarse {t(lambda: G.apply_coarse(v, y)):.4f} ms", flush=True)
+G.close()
