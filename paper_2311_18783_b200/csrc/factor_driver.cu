@@ -380,7 +380,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
   if (getenv("MDD_SWEEP_TRACE")) {
-    trace.alloc((size_t)2 * nphases * sweep_grid);
+    trace.alloc((size_t)dev::kTraceWords * nphases * sweep_grid);
     CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
   }
   if (getenv("MDD_PLAN_STATS")) {
@@ -459,8 +459,8 @@ DevFactor::~DevFactor() {
         cudaMemcpy(phh.data(), phases.p, phh.size() * sizeof(int4), cudaMemcpyDeviceToHost) == cudaSuccess) {
       std::string path = std::string(getenv("MDD_SWEEP_TRACE")) + "/trace_" + name + ".bin";
       if (FILE* f = fopen(path.c_str(), "wb")) {
-        int hdr[2] = {nphases, sweep_grid};
-        fwrite(hdr, sizeof(int), 2, f);
+        int hdr[3] = {nphases, sweep_grid, dev::kTraceWords};
+        fwrite(hdr, sizeof(int), 3, f);
         fwrite(phh.data(), sizeof(int4), phh.size(), f);
         fwrite(v.data(), 8, v.size(), f);
         fclose(f);

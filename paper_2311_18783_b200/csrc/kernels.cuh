@@ -100,6 +100,9 @@ constexpr int kStages = 2;       // tile ring slots per CTA (one tile streams wh
 constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can span)
 constexpr int kDescAhead = 4;    // M-task descriptors streamed ahead of the current task
 constexpr int kDescRing = 8;     // descriptor ring slots (> kDescAhead)
+// MDD_SWEEP_TRACE words per (phase, CTA): start, end (%globaltimer, thread 0),
+// time thread 0 waited on tile mbarriers, tiles consumed
+constexpr int kTraceWords = 4;
 constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
 
 // one task of an M phase (factor_driver.cu builds them, forward and backward)

@@ -4,9 +4,9 @@ import sys, struct
 import numpy as np
 path = sys.argv[1]
 with open(path, "rb") as f:
-    nph, grid = struct.unpack("ii", f.read(8))
+    nph, grid, words = struct.unpack("iii", f.read(12))
     ph = np.frombuffer(f.read(16 * nph), dtype=np.int32).reshape(nph, 4)
-    tr = np.frombuffer(f.read(16 * nph * grid), dtype=np.uint64).reshape(nph, grid, 2).astype(np.int64)
+    tr = np.frombuffer(f.read(8 * words * nph * grid), dtype=np.uint64).reshape(nph, grid, words).astype(np.int64)
 t0 = tr[tr > 0].min()
 names = ["G_f", "M_f", "G_b", "M_b", "prol"]
 tot = {}
@@ -20,6 +20,9 @@ for p in range(nph):
     gap = (s.min() - prev_end) / 1e3
     prev_end = e.max()
     tot[k] = tot.get(k, 0) + span
+    wait = np.median(tr[p, :, 2]) / 1e3
+    tiles = np.median(tr[p, :, 3])
     print(f"  {p:3d} {k:5s} [{ph[p,1]:8d},{ph[p,2]:8d}) start {s.min()/1e3:8.1f} end {e.max()/1e3:8.1f}"
-          f"  span {span:7.1f}  cta-median {work:6.1f}  barrier-gap {gap:5.1f} us")
+          f"  span {span:7.1f}  cta-median {work:6.1f} (tile-wait {wait:5.1f}, tiles {tiles:4.0f})"
+          f"  barrier-gap {gap:5.1f} us")
 print("  totals:", {k: round(v, 1) for k, v in tot.items()})
