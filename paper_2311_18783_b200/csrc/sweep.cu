@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     const int4 PH = S.phases[ph];
     const int kind = PH.x;
     const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
+    unsigned long long t_wait = 0, t_tiles = 0;  // trace: thread 0's time in tile waits, tiles
     if (kind == PH_GF) {
       // t = [b_c ; 0] + children's updates, one row per thread
       for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_t(S, q);
@@ -505,7 +506,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         // wait for the next tile of the stream (its ring slot becomes `buf`)
         auto next_tile_and_wait = [&](int) {
           buf = cs % kStages;
+          const unsigned long long w0 = (S.trace && tid == 0) ? globaltimer() : 0ull;
           mbar_wait(&mbar[buf], (parbits >> buf) & 1u);
+          if (S.trace && tid == 0) { t_wait += globaltimer() - w0; ++t_tiles; }
           parbits ^= 1u << buf;
         };
         // after the tile's last read (callers __syncthreads first): refill its slot
@@ -644,8 +647,11 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     // order this thread's generic-proxy global writes before them
     asm volatile("fence.proxy.async.global;" ::: "memory");
     if (S.trace && tid == 0) {
-      S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x)] = t_ph;
-      S.trace[2 * ((size_t)ph * gridDim.x + blockIdx.x) + 1] = globaltimer();
+      unsigned long long* tr = S.trace + kTraceWords * ((size_t)ph * gridDim.x + blockIdx.x);
+      tr[0] = t_ph;
+      tr[1] = globaltimer();
+      tr[2] = t_wait;
+      tr[3] = t_tiles;
     }
     if (ph + 1 < S.nphases)
       grid_barrier(S.ctl, ((cur - 1) * (unsigned long long)(S.nphases - 1) + ph + 1) * grid);
