@@ -127,12 +127,38 @@ __device__ __forceinline__ void tile_matvec(const double* T, int R, int C, const
     }
     return;
   }
-  // rows per slice group: a multiple of 32, or a power of two below 32
-  const int Rp = R >= 32 ? (R + 31) & ~31 : (R > 16 ? 32 : R > 8 ? 16 : R > 4 ? 8 : R > 2 ? 4 : R);
-  const int nsl = min(kSweepThreads / Rp, C);
-  const int i = tid % Rp, sl = tid / Rp;
-  if (sl < nsl && i < R) {
-    const int ja = (sl * C) / nsl, jb = ((sl + 1) * C) / nsl;
+  if (R <= 16) {
+    // few rows (a fwd strip of a wide supernode): R-row slices over the columns
+    const int Rp = R > 8 ? 16 : R > 4 ? 8 : R > 2 ? 4 : R;
+    const int nsl = min(kSweepThreads / Rp, C);
+    const int i = tid % Rp, sl = tid / Rp;
+    if (sl < nsl && i < R) {
+      const int ja = (sl * C) / nsl, jb = ((sl + 1) * C) / nsl;
+      double s0 = 0.0, s1 = 0.0;
+      int j = ja;
+      for (; j + 2 <= jb; j += 2) {
+        s0 += T[j * R + i] * v[j];
+        s1 += T[(j + 1) * R + i] * v[j + 1];
+      }
+      if (j < jb) s0 += T[j * R + i] * v[j];
+      red[sl * Rp + i] = s0 + s1;
+    }
+    __syncthreads();
+    if (tid < R) {
+      double s = 0.0;
+      for (int q = 0; q < nsl; ++q) s += red[q * Rp + tid];
+      fin(tid, s);
+    }
+    return;
+  }
+  // 16 < R <= 128: 2^lg rows per slice, 2^(8-lg) column slices; all index math
+  // in shifts (no integer division on the per-tile path)
+  static_assert(kSweepThreads == 256, "slice mapping assumes 256 threads");
+  const int lg = R <= 32 ? 5 : R <= 64 ? 6 : 7;
+  const int lgs = min(8 - lg, C > 1 ? 32 - __clz(C - 1) : 0);  // no more slices than columns
+  const int i = tid & ((1 << lg) - 1), sl = tid >> lg;
+  if (i < R && sl < (1 << lgs)) {
+    const int ja = (sl * C) >> lgs, jb = ((sl + 1) * C) >> lgs;
     double s0 = 0.0, s1 = 0.0;
     int j = ja;
     for (; j + 2 <= jb; j += 2) {
@@ -140,12 +166,12 @@ __device__ __forceinline__ void tile_matvec(const double* T, int R, int C, const
       s1 += T[(j + 1) * R + i] * v[j + 1];
     }
     if (j < jb) s0 += T[j * R + i] * v[j];
-    red[sl * Rp + i] = s0 + s1;
+    red[tid] = s0 + s1;  // slice sl, row i
   }
   __syncthreads();
   if (tid < R) {
     double s = 0.0;
-    for (int q = 0; q < nsl; ++q) s += red[q * Rp + tid];
+    for (int q = 0; q < (1 << lgs); ++q) s += red[(q << lg) + tid];
     fin(tid, s);
   }
 }
@@ -275,11 +301,12 @@ __device__ __forceinline__ void tile_matvec_packed(const double* T, int nr, int 
     }
     return;
   }
-  const int Rp = R >= 32 ? (R + 31) & ~31 : (R > 16 ? 32 : R > 8 ? 16 : R > 4 ? 8 : R > 2 ? 4 : R);
-  const int nsl = max(1, min(kSweepThreads / Rp, C));
-  const int ip = tid % Rp, sl = tid / Rp;
-  if (sl < nsl && ip < R) {
-    const int ja = (sl * C) / nsl, jb = min(((sl + 1) * C) / nsl, ip + 1);
+  // 2^lg rows per slice, 2^(8-lg) column slices (shifts only)
+  const int lg = R <= 4 ? 2 : R <= 8 ? 3 : R <= 16 ? 4 : R <= 32 ? 5 : R <= 64 ? 6 : 7;
+  const int lgs = min(8 - lg, C > 1 ? 32 - __clz(C - 1) : 0), Rp = 1 << lg, nsl = 1 << lgs;
+  const int ip = tid & (Rp - 1), sl = tid >> lg;
+  if (ip < R && sl < nsl) {
+    const int ja = (sl * C) >> lgs, jb = min(((sl + 1) * C) >> lgs, ip + 1);
     double s0 = 0.0;
     // address of (row c0+ip, column jj): coff(jj) + ip - jj
     int addr = ja * R - (ja * (ja - 1)) / 2 + ip - ja;
