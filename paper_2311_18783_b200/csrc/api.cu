@@ -958,7 +958,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
             }
           }
           if (ki > 0)
-            for (int r0 = 0; r0 < ni; r0 += 256) bz.push_back(make_int4(i, r0, 0, 0));
+            for (int r0 = 0; r0 < ni; r0 += dev::kGeneoZRows) bz.push_back(make_int4(i, r0, 0, 0));
           wtot += (int64_t)ni * ki;
           gcol += ki;
         }

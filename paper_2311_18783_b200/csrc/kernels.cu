@@ -569,7 +569,8 @@ __global__ void k_geneo_zt2(int ncols, const int* __restrict__ cblk, const int* 
 }
 
 // u[off_i + p] = sum_k W_i[p + k n_i] xc[gpos[gcol0_i + k]]  (rows of subdomain i);
-// the block's k_i coarse values are staged in shared memory (64 at a time)
+// the block's k_i coarse values are staged in shared memory (64 at a time); each
+// thread owns kGeneoZRows / 256 rows (all their loads of a column chunk in flight)
 __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                                                  const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                                                  const int* __restrict__ kcnt, const int* __restrict__ gcol0,
@@ -577,34 +578,51 @@ __global__ void __launch_bounds__(256) k_geneo_z(const int4* __restrict__ blk, c
                                                  const double* __restrict__ xc, double* __restrict__ u,
                                                  const int* __restrict__ stop) {
   if (STOPPED) return;
+  constexpr int RPT = kGeneoZRows / 256;
   __shared__ double xs[64];
   const int4 b = blk[blockIdx.x];  // {subdomain, first row, -, -}
   const int i = b.x;
   const int ni = nsz[i], ki = kcnt[i];
-  const int p = b.y + threadIdx.x;
-  const bool act = p < ni;
   const double* Wi = W + woff[i];
   const int32_t* gp = gpos + gcol0[i];
-  // eight independent column streams in flight per thread; column k goes to s[k % 8]
-  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  // per row: eight column streams; column k goes to s[t][k % 8]
+  double s[RPT][8];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[t][j] = 0.0;
   for (int kb = 0; kb < ki; kb += 64) {
     const int kn = min(64, ki - kb);
     __syncthreads();
     if (threadIdx.x < kn) xs[threadIdx.x] = __ldg(xc + __ldg(gp + kb + threadIdx.x));
     __syncthreads();
-    if (act) {
-      int k = 0;
-      for (; k + 8 <= kn; k += 8) {
-        double w[8];
+    int k = 0;
+    for (; k + 8 <= kn; k += 8) {
+      double w[RPT][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) w[j] = __ldcs(Wi + (int64_t)(kb + k + j) * ni + p);
+      for (int t = 0; t < RPT; ++t) {
+        const int p = b.y + t * 256 + (int)threadIdx.x;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) s[j] += w[j] * xs[k + j];
+        for (int j = 0; j < 8; ++j) w[t][j] = p < ni ? __ldcs(Wi + (int64_t)(kb + k + j) * ni + p) : 0.0;
       }
-      for (int j = 0; k < kn; ++k, ++j) s[j] += __ldcs(Wi + (int64_t)(kb + k) * ni + p) * xs[k];
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s[t][j] += w[t][j] * xs[k + j];
     }
+    for (int j = 0; k < kn; ++k, ++j)
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int p = b.y + t * 256 + (int)threadIdx.x;
+        if (p < ni) s[t][j] += __ldcs(Wi + (int64_t)(kb + k) * ni + p) * xs[k];
+      }
   }
-  if (act) u[poff[i] + p] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int p = b.y + t * 256 + (int)threadIdx.x;
+    if (p < ni)
+      u[poff[i] + p] = ((s[t][0] + s[t][1]) + (s[t][2] + s[t][3])) + ((s[t][4] + s[t][5]) + (s[t][6] + s[t][7]));
+  }
 }
 
 // out[e] = Z_g(e, :) xc + sum of the GenEO contributions u at the copies of e

@@ -207,7 +207,8 @@ MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
 MDD_SPMV_G_DECL(k_spmv32)
 #undef MDD_SPMV_G_DECL
-constexpr int kGeneoRows = 1024;  // rows per block of the Z_e^T v reduction
+constexpr int kGeneoRows = 1024;  // rows per block of the Z_e^T v reduction (2048: slower)
+constexpr int kGeneoZRows = 512;  // rows per block of W_i y_i (2 per thread: one wave on c1)
 __global__ void k_geneo_zt(const int4* __restrict__ blk, const int64_t* __restrict__ woff,
                            const int64_t* __restrict__ poff, const int* __restrict__ nsz,
                            const int* __restrict__ gcol0, const int32_t* __restrict__ gpos,
