@@ -213,6 +213,11 @@ struct mdd_solver {
   // PCG work
   DBuf<double> x, r, p, q, z, t1, t2, t3, t4, xloc, xc, S, part;
   DBuf<int> state;
+  DBuf<unsigned int> red_counter;  // last-block counter of the fused reduction tails (re-armed by them)
+  // a reduction tail: S[slot] = sum of the producing kernel's block partials, then
+  // the CG scalar step op, by its last block
+  dev::RedStep rstep(int slot, int op) { return dev::RedStep{S.p, state.p, red_counter.p, slot, op}; }
+  static dev::RedStep rnone() { return dev::RedStep{nullptr, nullptr, nullptr, 0, 0}; }
   int* state_host = nullptr;
   int nparts = 0;
   std::vector<double> setup_times;
@@ -265,13 +270,14 @@ struct mdd_solver {
   // A x with 8 lanes per row on an SM-sized grid (nparts blocks: the fused dot's
   // partials are reduced by one small kernel)
   void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
-            double* out, const double* dotw = nullptr, double* part_ = nullptr, const double* sub = nullptr) {
+            double* out, const double* dotw = nullptr, double* part_ = nullptr, const double* sub = nullptr,
+            dev::RedStep rs = rnone()) {
     if (spmv_tpr == 4)
-      dev::k_spmv4<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+      dev::k_spmv4<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p, rs);
     else if (spmv_tpr == 16)
-      dev::k_spmv16<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+      dev::k_spmv16<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p, rs);
     else
-      dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p);
+      dev::k_spmv8<<<nparts, 256, 0, stream>>>(rows, ptr, idx, val, in, sub, out, dotw, part_, state.p, rs);
     launches += 1;
   }
   void applyA(const double* in, double* out) {
@@ -289,10 +295,11 @@ struct mdd_solver {
   // the sweep on E, then Z_g xc + prolongation of the GenEO blocks' W_i xc_i
   // (addw, dotw: y = addw + Q v and dotw . y partials into part, fused into the
   // last kernel; used by the PCG loop's coarse-start form)
-  void apply_coarse(const double* v, double* y, const double* addw = nullptr, const double* dotw = nullptr) {
+  void apply_coarse(const double* v, double* y, const double* addw = nullptr, const double* dotw = nullptr,
+                    dev::RedStep rs = rnone()) {
     prof_begin(MDD_PROF_COARSE);
     dev::k_spmv32<<<nparts, 256, 0, stream>>>((int)n0, Zgt_ptr.p, Zgt_idx.p, Zgt_val.p, v, nullptr, xc.p,
-                                              nullptr, nullptr, state.p);
+                                              nullptr, nullptr, state.p, rnone());
     if (nbzt) {
       dev::k_geneo_zt<<<nbzt, 256, 0, stream>>>(W_bzt.p, W_off.p, W_poff.p, W_n.p, W_gc0.p, W_gpos.p, W_val.p,
                                                 gmap.p, v, W_part.p, state.p);
@@ -305,7 +312,7 @@ struct mdd_solver {
                                               W_val.p, crs.xb.p, u_loc.p, state.p);
     dev::k_z_apply<<<nparts, 256, 0, stream>>>(n, Zg_ptr.p, Zg_idx.p, Zg_val.p, crs.xb.p, pro_ptr.p, pro_pos.p,
                                               nbz ? u_loc.p : nullptr, addw, y, dotw, dotw ? part.p : nullptr,
-                                              state.p);
+                                              state.p, rs);
     prof_end();
     launches += 3 + (nbzt ? 2 : 0) + (nbz ? 1 : 0);
   }
@@ -335,29 +342,29 @@ struct mdd_solver {
   bool coarse_start() const { return has_coarse && desc.variant == MDD_VARIANT_AS2_COARSE_START; }
   // the preconditioner inside the PCG loop: for the coarse start (Z^T r = 0,
   // reading R13) eq. (2.4) is z = w + Q (r - A w), w = M_AS r
-  void apply_prec_loop(const double* rr, double* zz) {
+  // (rs: the r . z reduction tail the coarse-start form runs inside its last kernel)
+  void apply_prec_loop(const double* rr, double* zz, dev::RedStep rs = rnone()) {
     if (!coarse_start()) {
       apply_prec(rr, zz);
       return;
     }
     apply_local(rr, t4.p);                                         // w = M_AS r
     spmv(A_ptr.p, A_idx.p, A_val.p, n, t4.p, t3.p, nullptr, nullptr, rr);  // r - A w
-    apply_coarse(t3.p, zz, t4.p, rr);   // z = w + Q (r - A w), with the r . z partials
+    apply_coarse(t3.p, zz, t4.p, rr, rs);   // z = w + Q (r - A w), with the r . z partials
   }
   // r . z after apply_prec_loop: the coarse-start form left its partials in part
+  // (the coarse-start loop already reduced it inside apply_prec_loop)
   void dot_rz(int slot, int op) {
-    if (!coarse_start()) {
-      dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, z.p, part.p, state.p);
-      launches += 1;
-    }
-    reduce_step(slot, op);
+    if (coarse_start()) return;
+    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, z.p, part.p, state.p, rstep(slot, op));
+    launches += 1;
   }
   void check_aborts() {
     loc.check_abort(stream);
     if (has_coarse) crs.check_abort(stream);
   }
   void dot(const double* a, const double* b, int slot) {
-    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p);
+    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p, rnone());
     dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
     launches += 2;
   }
@@ -369,9 +376,8 @@ struct mdd_solver {
   // ---------------------------------------------------------------- PCG
   // prologue (x = 0 and r = f staged by the host): ||f||, z = M r, p = z, rz
   void enqueue_prologue() {
-    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, r.p, part.p, state.p);
+    dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, r.p, r.p, part.p, state.p, rstep(dev::S_RR, 3));
     launches += 1;
-    reduce_step(dev::S_RR, 3);
     if (coarse_start()) {
       // x0 = Q f, r0 = f - A x0 (the staged x is 0; reading R13)
       apply_coarse(r.p, x.p);
@@ -388,14 +394,13 @@ struct mdd_solver {
   // marks: optional event indices for the eager profiling path
   void enqueue_body(const std::function<void(int)>& mark) {
     if (mark) mark(2);
-    spmv(A_ptr.p, A_idx.p, A_val.p, n, p.p, q.p, p.p, part.p);
+    spmv(A_ptr.p, A_idx.p, A_val.p, n, p.p, q.p, p.p, part.p, nullptr, rstep(dev::S_PQ, 0));
     if (mark) mark(3);
-    reduce_step(dev::S_PQ, 0);
-    dev::k_update_xr<<<nparts, 256, 0, stream>>>(n, x.p, r.p, p.p, q.p, S.p, part.p, state.p);
+    dev::k_update_xr<<<nparts, 256, 0, stream>>>(n, x.p, r.p, p.p, q.p, S.p, part.p, state.p,
+                                                 rstep(dev::S_RR, 1));
     launches += 1;
-    reduce_step(dev::S_RR, 1);
     if (mark) mark(4);
-    apply_prec_loop(r.p, z.p);
+    apply_prec_loop(r.p, z.p, rstep(dev::S_RZNEW, 2));
     if (mark) mark(5);
     dot_rz(dev::S_RZNEW, 2);
     dev::k_update_p<<<nparts, 256, 0, stream>>>(n, p.p, z.p, S.p, state.p);
@@ -1004,6 +1009,8 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
   H->part.alloc(std::max<int64_t>(H->nparts, nblk(n, 8)) + 8);
   H->state.alloc(dev::ST_COUNT);
   H->state.zero(s);
+  H->red_counter.alloc(1);
+  H->red_counter.zero(s);
   CUDA_CHECK(cudaMallocHost(&H->state_host, dev::ST_COUNT * sizeof(int)));
   CUDA_CHECK(cudaMallocHost(&H->host_S, dev::S_COUNT * sizeof(double)));
   CUDA_CHECK(cudaMallocHost(&H->host_state, dev::ST_COUNT * sizeof(int)));

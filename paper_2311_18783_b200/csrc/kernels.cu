@@ -405,7 +405,8 @@ __global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t*
 #define STOPPED (stop != nullptr && stop[0] != 0)
 
 // block-level sum of one value per thread -> part[blockIdx.x]; blockDim = 256
-__device__ __forceinline__ void block_sum_store(double v, double* part) {
+// block-level sum of one value per thread -> *dst (thread 0); blockDim = 256
+__device__ __forceinline__ void block_sum_to(double v, double* dst) {
   __shared__ double ws[32];
   v = warp_sum(v);
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -415,7 +416,34 @@ __device__ __forceinline__ void block_sum_store(double v, double* part) {
     int nw = blockDim.x >> 5;
     double s = lane < nw ? ws[lane] : 0.0;
     s = warp_sum(s);
-    if (lane == 0) part[blockIdx.x] = s;
+    if (lane == 0) *dst = s;
+  }
+}
+__device__ __forceinline__ void block_sum_store(double v, double* part) { block_sum_to(v, part + blockIdx.x); }
+
+__device__ void scalar_op(int op, double* __restrict__ S, int* __restrict__ state);
+
+// RedStep tail (see kernels.cuh): call after block_sum_store(..., part)
+__device__ void reduce_step_tail(const double* part, const RedStep& rs) {
+  if (!rs.counter) return;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(rs.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(part + i);
+  __shared__ double tmp[1];
+  block_sum_to(s, tmp);  // (not block_sum_store: this block's index is not 0)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    rs.S[rs.slot] = tmp[0];
+    scalar_op(rs.op, rs.S, rs.state);
+    *rs.counter = 0u;
   }
 }
 
@@ -449,7 +477,7 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
                                                 const double* __restrict__ x,
                                                 const double* __restrict__ sub, double* __restrict__ y,
                                                 const double* __restrict__ dotw, double* __restrict__ part,
-                                                const int* __restrict__ stop) {
+                                                const int* __restrict__ stop, const RedStep& rs) {
   if (STOPPED) return;
   const int g = (blockIdx.x * blockDim.x + threadIdx.x) / TPR;
   const int lane = threadIdx.x & (TPR - 1);
@@ -478,15 +506,18 @@ __device__ __forceinline__ void spmv_g_body(int nrows, const int64_t* __restrict
       if (dotw) dsum += dotw[row] * s;
     }
   }
-  if (part) block_sum_store(dsum, part);
+  if (part) {
+    block_sum_store(dsum, part);
+    reduce_step_tail(part, rs);
+  }
 }
 #define MDD_SPMV_G(NAME, TPR)                                                                      \
   __global__ void __launch_bounds__(256)                                                           \
       NAME(int nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,          \
            const double* __restrict__ val, const double* __restrict__ x,                          \
            const double* __restrict__ sub, double* __restrict__ y, const double* __restrict__ dotw, \
-           double* __restrict__ part, const int* __restrict__ stop) {                              \
-    spmv_g_body<TPR>(nrows, ptr, idx, val, x, sub, y, dotw, part, stop);                          \
+           double* __restrict__ part, const int* __restrict__ stop, RedStep rs) {                  \
+    spmv_g_body<TPR>(nrows, ptr, idx, val, x, sub, y, dotw, part, stop, rs);                      \
   }
 MDD_SPMV_G(k_spmv4, 4)
 MDD_SPMV_G(k_spmv8, 8)
@@ -632,7 +663,7 @@ __global__ void __launch_bounds__(256) k_z_apply(int n, const int64_t* __restric
                                                  const int32_t* __restrict__ ppos, const double* __restrict__ u,
                                                  const double* __restrict__ addw, double* __restrict__ out,
                                                  const double* __restrict__ dotw, double* __restrict__ part,
-                                                 const int* __restrict__ stop) {
+                                                 const int* __restrict__ stop, RedStep rs) {
   if (STOPPED) return;
   double d = 0.0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
@@ -644,16 +675,20 @@ __global__ void __launch_bounds__(256) k_z_apply(int n, const int64_t* __restric
     out[e] = s;
     if (dotw) d += dotw[e] * s;  // the same per-thread order as k_dot_part
   }
-  if (part) block_sum_store(d, part);
+  if (part) {
+    block_sum_store(d, part);
+    reduce_step_tail(part, rs);
+  }
 }
 
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
-                           double* __restrict__ part, const int* __restrict__ stop) {
+                           double* __restrict__ part, const int* __restrict__ stop, RedStep rs) {
   if (STOPPED) return;
   double s = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     s += a[i] * b[i];
   block_sum_store(s, part);
+  reduce_step_tail(part, rs);
 }
 
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
@@ -662,7 +697,7 @@ __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
   __shared__ double tmp[1];
-  block_sum_store(s, tmp);
+  block_sum_to(s, tmp);
   __syncthreads();
   if (threadIdx.x == 0) *out = tmp[0];
 }
@@ -709,7 +744,7 @@ __global__ void k_reduce_step(int nparts, const double* __restrict__ part, doubl
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
   __shared__ double tmp[1];
-  block_sum_store(s, tmp);
+  block_sum_to(s, tmp);
   __syncthreads();
   if (threadIdx.x == 0) {
     S[slot] = tmp[0];
@@ -725,7 +760,7 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict_
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
                             const double* __restrict__ p, const double* __restrict__ q,
                             const double* __restrict__ S, double* __restrict__ part,
-                            const int* __restrict__ stop) {
+                            const int* __restrict__ stop, RedStep rs) {
   if (STOPPED) return;
   const double alpha = S[S_ALPHA];
   double s = 0.0;
@@ -736,6 +771,7 @@ __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ 
     s += ri * ri;
   }
   block_sum_store(s, part);
+  reduce_step_tail(part, rs);
 }
 
 __global__ void k_update_p(int n, double* __restrict__ p, const double* __restrict__ z,

@@ -194,6 +194,16 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
                        const double* __restrict__ val, const double* __restrict__ x,
                        double* __restrict__ y, const double* __restrict__ dotw,
                        double* __restrict__ part, const int* __restrict__ stop);
+// optional tail of a kernel that leaves one partial sum per block: the last block
+// to finish adds the partials in the order of k_reduce_step (same bits), stores
+// S[slot], runs the CG scalar step `op` and re-arms the counter (counter == null:
+// no tail)
+struct RedStep {
+  double* S;
+  int* state;
+  unsigned int* counter;
+  int slot, op;
+};
 // y = M x (or y = sub - M x), 8 / 16 / 32 lanes per row on an SM-sized grid,
 // optional fused dot partials of dotw . y
 #define MDD_SPMV_G_DECL(NAME)                                                                    \
@@ -201,7 +211,7 @@ __global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __
                        const double* __restrict__ val, const double* __restrict__ x,                \
                        const double* __restrict__ sub, double* __restrict__ y,                      \
                        const double* __restrict__ dotw, double* __restrict__ part,                  \
-                       const int* __restrict__ stop);
+                       const int* __restrict__ stop, RedStep rs);
 MDD_SPMV_G_DECL(k_spmv4)
 MDD_SPMV_G_DECL(k_spmv8)
 MDD_SPMV_G_DECL(k_spmv16)
@@ -227,9 +237,9 @@ __global__ void k_z_apply(int n, const int64_t* __restrict__ ptr, const int32_t*
                           const int64_t* __restrict__ pptr, const int32_t* __restrict__ ppos,
                           const double* __restrict__ u, const double* __restrict__ addw,
                           double* __restrict__ out, const double* __restrict__ dotw,
-                          double* __restrict__ part, const int* __restrict__ stop);
+                          double* __restrict__ part, const int* __restrict__ stop, RedStep rs);
 __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
-                           double* __restrict__ part, const int* __restrict__ stop);
+                           double* __restrict__ part, const int* __restrict__ stop, RedStep rs);
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
                          const int* __restrict__ stop);
 __global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state);
@@ -239,7 +249,7 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict_
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
                             const double* __restrict__ p, const double* __restrict__ q,
                             const double* __restrict__ S, double* __restrict__ part,
-                            const int* __restrict__ stop);
+                            const int* __restrict__ stop, RedStep rs);
 __global__ void k_update_p(int n, double* __restrict__ p, const double* __restrict__ z,
                            const double* __restrict__ S, const int* __restrict__ stop);
 __global__ void k_axpby(int n, double a, const double* __restrict__ x, double b,
