@@ -268,7 +268,7 @@ struct mdd_solver {
 
   // ------------------------------------------------------------ helpers
   // A x with 8 lanes per row on an SM-sized grid (nparts blocks: the fused dot's
-  // partials are reduced by one small kernel)
+  // partials are reduced by the kernel's last block when rs is given)
   void spmv(const int64_t* ptr, const int32_t* idx, const double* val, int rows, const double* in,
             double* out, const double* dotw = nullptr, double* part_ = nullptr, const double* sub = nullptr,
             dev::RedStep rs = rnone()) {
@@ -367,11 +367,6 @@ struct mdd_solver {
     dev::k_dot_part<<<nparts, 256, 0, stream>>>(n, a, b, part.p, state.p, rnone());
     dev::k_reduce<<<1, 256, 0, stream>>>(nparts, part.p, S.p + slot, state.p);
     launches += 2;
-  }
-  // S[slot] = reduced partials, then the CG scalar step `op`, in one launch
-  void reduce_step(int slot, int op) {
-    dev::k_reduce_step<<<1, 256, 0, stream>>>(nparts, part.p, S.p, slot, op, state.p);
-    launches += 1;
   }
   // ---------------------------------------------------------------- PCG
   // prologue (x = 0 and r = f staged by the host): ||f||, z = M r, p = z, rz
