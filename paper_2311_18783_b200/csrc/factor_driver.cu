@@ -181,9 +181,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     X.vbytes = (int)((((hi - X.vlo2) + 1) & ~1LL) * (int64_t)sizeof(double));
     X.vn = (int)(hi - lo);
   };
-  // the fixed cost of one M task in byte equivalents (~1.5 us of one CTA's
-  // streaming rate: task start, partial-sum store, atomic)
-  const int64_t kTaskCostBytes = getenv("MDD_TASK_COST") ? atoll(getenv("MDD_TASK_COST")) : 24 * 1024;
+  // the fixed cost of one M task in byte equivalents (measured best of 12-64 KB on c1;
+  // ~3 us of one CTA: task start, partial-sum store, atomic, combine)
+  const int64_t kTaskCostBytes = getenv("MDD_TASK_COST") ? atoll(getenv("MDD_TASK_COST")) : 48 * 1024;
   struct Cand {
     int64_t bytes;
     dev::MTaskDesc d;
