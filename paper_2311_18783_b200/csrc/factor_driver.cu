@@ -82,6 +82,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     return (int)tl.size() - 1;
   };
   const int64_t single_max = getenv("MDD_SINGLE_MAX") ? atoll(getenv("MDD_SINGLE_MAX")) : dev::kSingleMax;
+  const int env_cb = getenv("MDD_TILE_CB") ? std::max(8, atoi(getenv("MDD_TILE_CB"))) : 64;  // 2-D tile columns
   for (int g = 0; g < nsn; ++g) {
     const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
     // a supernode one CTA sweeps alone must stay short (it is a phase's critical path
@@ -108,7 +109,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     } else {
       // a task's vector (up to kGroup row blocks / column blocks) must fit a
       // kVecMax shared-memory slot: RB, CB <= kVecMax / kGroup
-      const int CB = std::min(nc, 64);
+      const int CB = std::min(nc, env_cb);
       const int RB = std::max(1, std::min(dev::kVecMax / 4, dev::kTileMax / CB));
       const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
