@@ -124,6 +124,17 @@ int mdd_apply_local(mdd_handle h, const double* r, double* z);
 /* y = Z E^{-1} Z^T v (coarse correction Q).  DEVICE pointers. */
 int mdd_apply_coarse(mdd_handle h, const double* v, double* y);
 
+/* Parity diagnostics (test infrastructure of the backward-error checks; not
+ * on the solve path).
+ * mdd_apply_local_parts: the local solutions x_i = A_i^{-1} R_i r of eq. (2.3)
+ * BEFORE the prolongation sum.  r: DEVICE, n doubles; xloc: DEVICE, MDD_INFO_NLOC
+ * doubles, subdomain-major, each block in N_i order (MDD_ARR_SUB_DOFS).
+ * mdd_apply_coarse_inverse: y = E^{-1} v for the factorised coarse matrix E
+ * (MDD_ARR_E_* / MDD_DARR_E_VAL, coarse-position order).  v, y: DEVICE,
+ * MDD_INFO_N0 doubles.  MDD_ERR_ARG without a coarse space. */
+int mdd_apply_local_parts(mdd_handle h, const double* r, double* xloc);
+int mdd_apply_coarse_inverse(mdd_handle h, const double* v, double* y);
+
 /* Integer / scalar facts about the handle (HOST array out[0..MDD_INFO_COUNT)). */
 enum {
   MDD_INFO_N = 0,           /* free edge dofs n                        */
@@ -149,6 +160,17 @@ enum {
                                threshold 1e-14 (kappa(E) ~ 1/eps; 0 = exact LDL^T)   */
   MDD_INFO_NNZ_ZG,          /* entries of the gradient (SNK / NK) part of Z        */
   MDD_INFO_NNZ_W,           /* entries of the dense GenEO blocks of Z              */
+  /* plan statistics: supernodes swept as packed small tasks / strips / 2-D tile
+   * groups, and fronts factorised by the blocked path (> 1024 rows; cuBLAS
+   * trailing updates), for the local factors and for E */
+  MDD_INFO_LOCAL_SN_PACKED,
+  MDD_INFO_LOCAL_SN_STRIP,
+  MDD_INFO_LOCAL_SN_2D,
+  MDD_INFO_LOCAL_BLOCKED_FRONTS,
+  MDD_INFO_COARSE_SN_PACKED,
+  MDD_INFO_COARSE_SN_STRIP,
+  MDD_INFO_COARSE_SN_2D,
+  MDD_INFO_COARSE_BLOCKED_FRONTS,
   MDD_INFO_COUNT
 };
 int mdd_info(mdd_handle h, int64_t* out, int count);
@@ -167,6 +189,9 @@ enum {
   MDD_ARR_GRAD_NODES_PTR,   /* nsub+1 offsets into MDD_ARR_GRAD_NODES     */
   MDD_ARR_GRAD_NODES,       /* per subdomain: free-node columns of G_i    */
   MDD_ARR_GENEO_COUNT,      /* nsub: GenEO vectors kept per subdomain     */
+  MDD_ARR_E_PTR,            /* CSR of the factorised coarse matrix E (the  */
+  MDD_ARR_E_IDX,            /* Jacobi-scaled S Z^T A Z S), rows/cols in coarse-position
+                               order (the order of mdd_apply_coarse_inverse) */
   MDD_ARR_COUNT
 };
 int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len);
@@ -185,6 +210,7 @@ enum {
   MDD_DARR_M_VAL,           /* M in the same pattern                      */
   MDD_DARR_GENEO_LAMBDA,    /* kept eigenvalues, subdomain-major          */
   MDD_DARR_SETUP_TIMES,     /* seconds per setup phase (see mdd_phase_name)*/
+  MDD_DARR_E_VAL,           /* values of E in MDD_ARR_E_IDX order          */
   MDD_DARR_COUNT
 };
 int mdd_get_double_array(mdd_handle h, int which, double* out, int64_t cap, int64_t* len);

@@ -22,11 +22,13 @@ INFO_NAMES = ["n", "nedges", "nfree_nodes", "nsub", "nnz_A", "nloc", "grad_candi
               "grad_rank", "ngeneo", "n0", "local_factor_nnz", "coarse_factor_nnz",
               "local_supernodes", "local_levels", "coarse_supernodes", "coarse_levels",
               "nnz_Z", "kernels_per_iter", "last_launches",
-              "coarse_perturbed", "nnz_Zg", "nnz_W"]
+              "coarse_perturbed", "nnz_Zg", "nnz_W",
+              "local_sn_packed", "local_sn_strip", "local_sn_2d", "local_blocked_fronts",
+              "coarse_sn_packed", "coarse_sn_strip", "coarse_sn_2d", "coarse_blocked_fronts"]
 INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, "A_ptr": 4,
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
-              "geneo_count": 10}
-DBL_ARRAYS = {"A_val": 0, "K_val": 1, "M_val": 2, "geneo_lambda": 3, "setup_times": 4}
+              "geneo_count": 10, "E_ptr": 11, "E_idx": 12}
+DBL_ARRAYS = {"A_val": 0, "K_val": 1, "M_val": 2, "geneo_lambda": 3, "setup_times": 4, "E_val": 5}
 PROF_NAMES = ["spmv", "local", "prec_other", "coarse", "vector", "total"]
 
 
@@ -42,7 +44,8 @@ class SetupDesc(C.Structure):
 # every symbol include/maxwell_dd.h declares (checked by tests/test_abi.py)
 EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_stream", "mdd_set_variant",
            "mdd_apply_preconditioner",
-           "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_info",
+           "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_apply_local_parts",
+           "mdd_apply_coarse_inverse", "mdd_info",
            "mdd_get_int_array", "mdd_topology_int_array", "mdd_get_double_array",
            "mdd_phase_name", "mdd_set_profiling", "mdd_sweep_timing", "mdd_profile", "mdd_last_error"]
 
@@ -66,6 +69,8 @@ def load() -> C.CDLL:
         "mdd_apply_operator": (C.c_int, [P, P, P]),
         "mdd_apply_local": (C.c_int, [P, P, P]),
         "mdd_apply_coarse": (C.c_int, [P, P, P]),
+        "mdd_apply_local_parts": (C.c_int, [P, P, P]),
+        "mdd_apply_coarse_inverse": (C.c_int, [P, P, P]),
         "mdd_info": (C.c_int, [P, lp, C.c_int]),
         "mdd_get_int_array": (C.c_int, [P, C.c_int, lp, C.c_int64, lp]),
         "mdd_topology_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, lp, C.c_int64, lp]),

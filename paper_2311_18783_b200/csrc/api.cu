@@ -210,6 +210,13 @@ struct mdd_solver {
   int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0, coarse_perturbed = 0;
   std::vector<int64_t> geneo_count;
   std::vector<double> geneo_lambda;
+  // parity diagnostics: the factorised (Jacobi-scaled) E in its original column
+  // order (sorted pattern + value slots into E_val) and, per subdomain-major local
+  // dof (sys_off[i] + k, k in N_i order), its position in the local factor
+  Csr E_pat;
+  std::vector<int64_t> E_slot;
+  DBuf<double> E_val;
+  DBuf<int64_t> loc_pos;
   // PCG work
   DBuf<double> x, r, p, q, z, t1, t2, t3, t4, xloc, xc, S, part;
   DBuf<int> state;
@@ -559,6 +566,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         pos[cur[H->dec.sub_dofs[i][k]]++] = fp.iperm_global[fp.sys_off[i] + k];
     H->pro_ptr.upload(pp);
     H->pro_pos.upload(pos);
+    H->loc_pos.upload(std::vector<int64_t>(fp.iperm_global.begin(), fp.iperm_global.end()));
     H->loc.upload(n, H->pro_ptr.p, H->pro_pos.p, &gm);
   }
   H->setup_times[PH_LOCAL_SYMBOLIC] = now_s() - t0;
@@ -797,8 +805,8 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       CUDA_CHECK(cudaGetLastError());
       CUDA_CHECK(cudaStreamSynchronize(s));
     }
-    Csr epat;
-    std::vector<int64_t> eslot;
+    Csr& epat = H->E_pat;
+    std::vector<int64_t>& eslot = H->E_slot;
     download_sorted(E, epat, eslot);
     // coordinates: node for gradient columns, box centre for GenEO columns
     std::vector<int32_t> exyz(3 * nb);
@@ -849,6 +857,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     H->crs.name = "coarse";
     H->crs.upload();
     H->coarse_perturbed = H->crs.factor(E.val.p, 2, kCoarsePivotTol, nullptr, s);
+    H->E_val = std::move(E.val);  // kept for the parity diagnostics (MDD_DARR_E_VAL)
     // hot-path copies of Z with columns relabelled to coarse positions
     {
       std::vector<int> zp(n + 1), zi(Z.nnz);
@@ -1205,6 +1214,34 @@ int mdd_apply_coarse(mdd_handle h, const double* v, double* y) {
   });
 }
 
+int mdd_apply_local_parts(mdd_handle h, const double* r, double* xloc) {
+  if (!h || !r || !xloc) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    CUDA_CHECK(cudaSetDevice(h->device));
+    h->state.zero(h->stream);
+    h->loc.sweep(r, nullptr, h->stream, h->state.p);   // x_i stays in the factor's positions
+    const int64_t nloc = h->loc.fp.ntot;
+    dev::k_gather<<<nblk(nloc, 256), 256, 0, h->stream>>>(nloc, h->loc_pos.p, h->loc.xb.p, xloc);
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+    h->check_aborts();
+  });
+}
+
+int mdd_apply_coarse_inverse(mdd_handle h, const double* v, double* y) {
+  if (!h || !v || !y) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    MDD_REQUIRE(h->has_coarse, 2, "no coarse space configured");
+    CUDA_CHECK(cudaSetDevice(h->device));
+    h->state.zero(h->stream);
+    h->crs.sweep(v, nullptr, h->stream, h->state.p);   // right-hand side indexed by position
+    CUDA_CHECK(cudaMemcpyAsync(y, h->crs.xb.p, h->n0 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaGetLastError());
+    h->check_aborts();
+  });
+}
+
 int mdd_info(mdd_handle h, int64_t* out, int count) {
   if (!h || !out) { g_err = "null argument"; return MDD_ERR_ARG; }
   int64_t v[MDD_INFO_COUNT] = {0};
@@ -1225,7 +1262,15 @@ int mdd_info(mdd_handle h, int64_t* out, int count) {
   v[MDD_INFO_COARSE_SUPERNODES] = h->has_coarse ? h->crs.fp.nsn : 0;
   v[MDD_INFO_COARSE_LEVELS] = h->has_coarse ? h->crs.fp.nlevels : 0;
   v[MDD_INFO_NNZ_Z] = h->nnzZ;
-  v[MDD_INFO_KERNELS_PER_ITER] = 0;
+  v[MDD_INFO_KERNELS_PER_ITER] = h->launches_body;
+  v[MDD_INFO_LOCAL_SN_PACKED] = h->loc.n_packed;
+  v[MDD_INFO_LOCAL_SN_STRIP] = h->loc.n_strip;
+  v[MDD_INFO_LOCAL_SN_2D] = h->loc.n_2d;
+  v[MDD_INFO_LOCAL_BLOCKED_FRONTS] = h->loc.n_blocked;
+  v[MDD_INFO_COARSE_SN_PACKED] = h->has_coarse ? h->crs.n_packed : 0;
+  v[MDD_INFO_COARSE_SN_STRIP] = h->has_coarse ? h->crs.n_strip : 0;
+  v[MDD_INFO_COARSE_SN_2D] = h->has_coarse ? h->crs.n_2d : 0;
+  v[MDD_INFO_COARSE_BLOCKED_FRONTS] = h->has_coarse ? h->crs.n_blocked : 0;
   v[MDD_INFO_LAST_LAUNCHES] = h->launches;
   v[MDD_INFO_COARSE_PERTURBED] = h->coarse_perturbed;
   v[MDD_INFO_NNZ_ZG] = h->nnzZg;
@@ -1251,6 +1296,38 @@ int mdd_topology_int_array(const mdd_setup_desc* d, int which, int64_t* out, int
     if (rc != MDD_OK) throw Error(rc, g_err);
   });
 }
+
+namespace {
+// E (as factorised) permuted to coarse-position order: CSR pattern and values
+void coarse_matrix_pos(mdd_handle h, std::vector<int64_t>* ptr, std::vector<int64_t>* idx,
+                       std::vector<double>* val) {
+  MDD_REQUIRE(h->has_coarse, 2, "no coarse space configured");
+  const Csr& E = h->E_pat;
+  const auto& ip = h->crs.fp.iperm_global;
+  const int64_t nb = E.nrows;
+  std::vector<int64_t> col_of_pos(nb);
+  for (int64_t c = 0; c < nb; ++c) col_of_pos[ip[c]] = c;
+  std::vector<double> ev;
+  if (val) ev = h->E_val.download();
+  std::vector<int64_t> p(nb + 1, 0), ix;
+  std::vector<double> vv;
+  std::vector<std::pair<int64_t, int64_t>> row;
+  for (int64_t q = 0; q < nb; ++q) {
+    const int64_t c = col_of_pos[q];
+    row.clear();
+    for (int64_t k = E.ptr[c]; k < E.ptr[c + 1]; ++k) row.push_back({ip[E.idx[k]], h->E_slot[k]});
+    std::sort(row.begin(), row.end());
+    for (auto& e : row) {
+      if (idx) ix.push_back(e.first);
+      if (val) vv.push_back(ev[e.second]);
+    }
+    p[q + 1] = p[q] + (int64_t)row.size();
+  }
+  if (ptr) *ptr = std::move(p);
+  if (idx) *idx = std::move(ix);
+  if (val) *val = std::move(vv);
+}
+}  // namespace
 
 int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len) {
   if (!h || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
@@ -1279,6 +1356,8 @@ int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_
         for (auto& D : h->grad_nodes) v.insert(v.end(), D.begin(), D.end());
         break;
       case MDD_ARR_GENEO_COUNT: v = h->geneo_count; break;
+      case MDD_ARR_E_PTR: coarse_matrix_pos(h, &v, nullptr, nullptr); break;
+      case MDD_ARR_E_IDX: coarse_matrix_pos(h, nullptr, &v, nullptr); break;
       default: throw Error(MDD_ERR_ARG, "unknown array");
     }
     *len = (int64_t)v.size();
@@ -1296,6 +1375,7 @@ int mdd_get_double_array(mdd_handle h, int which, double* out, int64_t cap, int6
       case MDD_DARR_M_VAL: v = h->M_val.download(); break;
       case MDD_DARR_GENEO_LAMBDA: v = h->geneo_lambda; break;
       case MDD_DARR_SETUP_TIMES: v = h->setup_times; break;
+      case MDD_DARR_E_VAL: coarse_matrix_pos(h, nullptr, nullptr, &v); break;
       default: throw Error(MDD_ERR_ARG, "unknown array");
     }
     *len = (int64_t)v.size();

@@ -84,6 +84,9 @@ struct DevFactor {
   DBuf<double> Lt, fpart, bpart, vb;
   DBuf<unsigned long long> rb_cnt, cb_cnt, ctl, trace;
   int nphases = 0, nphases_noprolong = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
+  // plan statistics (mdd_info): supernodes swept as packed / strip / 2-D tasks,
+  // fronts factorised by the blocked (cuBLAS trailing update) path
+  int n_packed = 0, n_strip = 0, n_2d = 0, n_blocked = 0;
   int64_t lt_size = 0;
   const int64_t* pro_ptr = nullptr;
   const int32_t* pro_pos = nullptr;

@@ -127,6 +127,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   }
   ntiles = (int)tl.size();
   lt_size = off;
+  n_packed = n_strip = n_2d = 0;
+  for (int g = 0; g < nsn; ++g) (mode[g] == 0 ? n_packed : mode[g] == 1 ? n_strip : n_2d)++;
   auto tile_bytes = [&](int t) {
     return (int)((((int64_t)rc[t].x * rc[t].y + 1) & ~1LL) * (int64_t)sizeof(double));
   };
@@ -529,6 +531,7 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
   std::vector<int> small_ptr(fp.nlevels + 1, 0);
   std::vector<std::vector<int>> big(fp.nlevels);
   int64_t wmax = 1;
+  int n_blocked_now = 0;
   for (int l = 0; l < fp.nlevels; ++l) {
     small_ptr[l] = (int)small_list.size();
     for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
@@ -536,6 +539,7 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
       const int nr = fp.sn_ncol[g] + fp.sn_noff[g];
       if (nr > kBigFront) {
         big[l].push_back(g);
+        ++n_blocked_now;
         wmax = std::max<int64_t>(wmax, (int64_t)nr * kPanel);
       } else {
         small_list.push_back(g);
@@ -543,6 +547,7 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
     }
   }
   small_ptr[fp.nlevels] = (int)small_list.size();
+  n_blocked = n_blocked_now;
   DBuf<int> dsmall;
   dsmall.upload(small_list.empty() ? std::vector<int>{0} : small_list);
   bool any_big = false;
@@ -558,8 +563,10 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
     CUSOLVER_OK(cusolverDnCreate(&cs));
     CUSOLVER_OK(cusolverDnSetStream(cs, s));
     W.alloc(wmax);
-    info.alloc(1);
+    info.alloc(std::max(n_blocked, 1));  // one trtri info word per blocked front
+    info.zero(s);
   }
+  int iblk = 0;
   try {
     for (int l = 0; l < fp.nlevels; ++l) {
       const int cnt = small_ptr[l + 1] - small_ptr[l];
@@ -594,7 +601,7 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
         if (trw.n < dws + 8) trw.alloc(dws + 8);
         std::vector<char> hbuf(std::max<size_t>(hws, 1));
         CUSOLVER_OK(cusolverDnXtrtri(cs, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_UNIT, nc, CUDA_R_64F, Lp, nr, trw.p,
-                                     dws, hbuf.data(), hws, info.p));
+                                     dws, hbuf.data(), hws, info.p + iblk++));
         if (no > 0) {
           const double one = 1.0;
           CUBLAS_OK(cublasDtrmm(cb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_UNIT, no, nc,
@@ -612,6 +619,10 @@ int DevFactor::factor(const double* src, int mode, double tol, uint8_t* dropped,
   }
   if (cb) cublasDestroy(cb);
   if (cs) cusolverDnDestroy(cs);
+  if (any_big) {
+    std::vector<int> ti = info.download();
+    for (int v : ti) MDD_REQUIRE(v == 0, 1, "triangular inverse (trtri) of a blocked front failed");
+  }
   int e = 0;
   CUDA_CHECK(cudaMemcpy(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (mode != 2) MDD_REQUIRE(e == 0, 3, "nonpositive pivot in an SPD factorisation");

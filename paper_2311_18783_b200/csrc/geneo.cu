@@ -128,6 +128,14 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
         CUSOLVER_CHECK(cusolverDnDpotrf_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, g, Sg.p, g, &lw));
         DBuf<double> work; work.alloc(std::max(lw, 1));
         CUSOLVER_CHECK(cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, g, Sg.p, g, work.p, lw, info.p));
+        {
+          // a singular gradient Gram G^T A_j G (e.g. an ungrounded component) must not
+          // silently give a garbage xi_0j
+          int pinfo = 0;
+          CUDA_CHECK(cudaMemcpyAsync(&pinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+          CUDA_CHECK(cudaStreamSynchronize(s));
+          MDD_REQUIRE(pinfo == 0, 3, "G_j^T A_j G_j is not SPD in subdomain " + std::to_string(j));
+        }
         Xt.alloc(g * n);
         CUBLAS_CHECK(cublasDgeam(cb, CUBLAS_OP_T, CUBLAS_OP_N, g, n, &one, W1.p, n, &zero, Xt.p, g, Xt.p, g));
         CUSOLVER_CHECK(cusolverDnDpotrs(cs, CUBLAS_FILL_MODE_LOWER, g, n, Sg.p, g, Xt.p, g, info.p));

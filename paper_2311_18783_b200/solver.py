@@ -40,13 +40,25 @@ def topology_array(w, name: str) -> np.ndarray:
     return out
 
 
-def _ptr(t) -> int:
-    """Device pointer of a contiguous float64 CUDA tensor."""
+def _ptr(t, n=None, device=None) -> int:
+    """Device pointer of a contiguous float64 CUDA tensor of n elements on the
+    handle's device (the C ABI reads / writes exactly n doubles)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
             and t.is_contiguous()):
         raise TypeError("expected a contiguous float64 CUDA tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"expected {n} elements, got {t.numel()}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"tensor on cuda:{t.device.index}, handle on cuda:{device}")
     return t.data_ptr()
+
+
+def _host(a, n, name):
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+            and a.size == n):
+        raise ValueError(f"{name}: expected a C-contiguous float64 array of {n} elements")
+    return a
 
 
 class MaxwellDD:
@@ -56,6 +68,7 @@ class MaxwellDD:
     def __init__(self, w, coarse="snk", variant="as2", device=0, geneo=True):
         self.w = w
         self.variant = variant
+        self.device = device
         d, keep = _desc(w, coarse, variant, device, geneo)
         h = C.c_void_p()
         L.check(L.lib().mdd_setup(C.byref(d), C.byref(h)))
@@ -105,13 +118,16 @@ class MaxwellDD:
     def solve(self, f, x, tol=1e-8, maxit=1000):
         it = C.c_int(0)
         rel = C.c_double(0.0)
-        rc = L.lib().mdd_solve(self._h, _ptr(f), _ptr(x), tol, maxit, C.byref(it), C.byref(rel))
+        rc = L.lib().mdd_solve(self._h, self._p(f), self._p(x), tol, maxit, C.byref(it), C.byref(rel))
         if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
             L.check(rc)
         return it.value, rel.value, rc == L.MDD_OK
 
+    def _p(self, t, n=None):
+        return _ptr(t, self.n if n is None else n, self.device)
+
     def solve_host(self, f: np.ndarray, tol=1e-8, maxit=1000):
-        f = np.ascontiguousarray(f, dtype=np.float64)
+        f = _host(np.ascontiguousarray(f, dtype=np.float64), self.n, "f")
         x = np.empty_like(f)
         it = C.c_int(0)
         rel = C.c_double(0.0)
@@ -139,6 +155,8 @@ class MaxwellDD:
 
     def solve_host_into(self, f: np.ndarray, x: np.ndarray, tol=1e-8, maxit=1000):
         """mdd_solve_host on caller-owned (e.g. pinned) float64 host arrays."""
+        _host(f, self.n, "f")
+        _host(x, self.n, "x")
         it = C.c_int(0)
         rel = C.c_double(0.0)
         dp = C.POINTER(C.c_double)
@@ -172,16 +190,33 @@ class MaxwellDD:
                 "precond_in_loop": loop, "iteration": loop + spmv + 8 * n * 7}
 
     def apply_preconditioner(self, r, z):
-        L.check(L.lib().mdd_apply_preconditioner(self._h, _ptr(r), _ptr(z)))
+        L.check(L.lib().mdd_apply_preconditioner(self._h, self._p(r), self._p(z)))
 
     def apply_operator(self, x, y):
-        L.check(L.lib().mdd_apply_operator(self._h, _ptr(x), _ptr(y)))
+        L.check(L.lib().mdd_apply_operator(self._h, self._p(x), self._p(y)))
 
     def apply_local(self, r, z):
-        L.check(L.lib().mdd_apply_local(self._h, _ptr(r), _ptr(z)))
+        L.check(L.lib().mdd_apply_local(self._h, self._p(r), self._p(z)))
 
     def apply_coarse(self, v, y):
-        L.check(L.lib().mdd_apply_coarse(self._h, _ptr(v), _ptr(y)))
+        L.check(L.lib().mdd_apply_coarse(self._h, self._p(v), self._p(y)))
+
+    # ------------------------------------------------ parity diagnostics
+    def apply_local_parts(self, r, xloc):
+        """xloc = concatenated A_i^{-1} R_i r (subdomain-major, N_i order)."""
+        L.check(L.lib().mdd_apply_local_parts(self._h, self._p(r), self._p(xloc, int(self.info["nloc"]))))
+
+    def apply_coarse_inverse(self, v, y):
+        """y = E^{-1} v for the factorised E, coarse-position order."""
+        n0 = int(self.info["n0"])
+        L.check(L.lib().mdd_apply_coarse_inverse(self._h, self._p(v, n0), self._p(y, n0)))
+
+    def coarse_matrix(self):
+        """The factorised (Jacobi-scaled) E as a scipy CSR matrix, coarse-position order."""
+        import scipy.sparse as sp
+        n0 = int(self.info["n0"])
+        return sp.csr_matrix((self.double_array("E_val"), self.int_array("E_idx"), self.int_array("E_ptr")),
+                             shape=(n0, n0))
 
     def set_profiling(self, on=True):
         L.check(L.lib().mdd_set_profiling(self._h, 1 if on else 0))

@@ -93,11 +93,14 @@ def _channels(n, nchan, width, contrast, rng):
     return val, tuple(chans)
 
 
-def _c1(seed=2, n=32, p=4):
+# contrast / gamma / logrange keyword overrides build the well-conditioned
+# variants of the recipes used by the literal-tolerance parity tests (same code
+# paths, contrast <= 1e2, gamma = 1e-2); the defaults are BASELINE's configs.
+def _c1(seed=2, n=32, p=4, contrast=1e4, gamma=1e-4):
     rng = np.random.default_rng(seed)
-    mu_inv_cube, chans = _channels(n, n // 4, 2, 1e4, rng)
+    mu_inv_cube, chans = _channels(n, n // 4, 2, contrast, rng)
     nc = n ** 3
-    return Workload("c1_cube32_channels", n, n, n, 1.0 / n, p, p, p, 1, 1e-4, 0.1,
+    return Workload("c1_cube32_channels", n, n, n, 1.0 / n, p, p, p, 1, gamma, 0.1,
                     np.ones(nc, np.uint8), _per_tet(mu_inv_cube), np.ones(6 * nc),
                     f_seed=seed + 1000, holes=())
 
@@ -139,36 +142,36 @@ def _holes(n, nholes, size, rng, max_tries=1000):
     return present.astype(np.uint8), tuple(desc)
 
 
-def _c2(seed=3, n=48, p=6, hole=8):
+def _c2(seed=3, n=48, p=6, hole=8, gamma=1e-6, logrange=2.0):
     rng = np.random.default_rng(seed)
     mask, holes = _holes(n, 2, hole, rng)
     ci, cj, ck = _cube_coords(n, n, n)
     s = n // p
     sub = (ci // s) + p * ((cj // s) + p * (ck // s))
-    mu = 10.0 ** rng.uniform(-2, 2, p ** 3)
-    ep = 10.0 ** rng.uniform(-2, 2, p ** 3)
-    return Workload("c2_cube48_holes", n, n, n, 1.0 / n, p, p, p, 1, 1e-6, 0.1,
+    mu = 10.0 ** rng.uniform(-logrange, logrange, p ** 3)
+    ep = 10.0 ** rng.uniform(-logrange, logrange, p ** 3)
+    return Workload("c2_cube48_holes", n, n, n, 1.0 / n, p, p, p, 1, gamma, 0.1,
                     mask, _per_tet(1.0 / mu[sub]), _per_tet(ep[sub]),
                     f_seed=seed + 1000, holes=holes)
 
 
-def _c3(seed=4, n=96, p=8):
+def _c3(seed=4, n=96, p=8, contrast=1e3, gamma=1e-3):
     rng = np.random.default_rng(seed)
     ci, cj, ck = _cube_coords(n, n, n)
     layer = (ck * 16) // n
-    mu_inv = np.where(layer % 2 == 0, 1.0, 1e3)
+    mu_inv = np.where(layer % 2 == 0, 1.0, contrast)
     nc = n ** 3
     eps = 10.0 ** rng.uniform(np.log10(0.5), np.log10(2.0), 6 * nc)
-    return Workload("c3_cube96_layers", n, n, n, 1.0 / n, p, p, p, 2, 1e-3, 0.1,
+    return Workload("c3_cube96_layers", n, n, n, 1.0 / n, p, p, p, 2, gamma, 0.1,
                     np.ones(nc, np.uint8), _per_tet(mu_inv), eps, f_seed=seed + 1000)
 
 
-def _c4(seed=5, ngpu=1, m=64, q=4):
+def _c4(seed=5, ngpu=1, m=64, q=4, contrast=1e4, gamma=1e-2):
     rng = np.random.default_rng(seed)
     nx, ny, nz = m * ngpu, m, m
     nc = nx * ny * nz
-    mu_inv = np.where(rng.random(nc) < 0.05, 1e4, 1.0)
-    return Workload(f"c4_weak{m}_x{ngpu}", nx, ny, nz, 1.0 / m, q * ngpu, q, q, 1, 1e-2, 0.1,
+    mu_inv = np.where(rng.random(nc) < 0.05, contrast, 1.0)
+    return Workload(f"c4_weak{m}_x{ngpu}", nx, ny, nz, 1.0 / m, q * ngpu, q, q, 1, gamma, 0.1,
                     np.ones(nc, np.uint8), _per_tet(mu_inv), np.ones(6 * nc),
                     f_seed=seed + 1000)
 
