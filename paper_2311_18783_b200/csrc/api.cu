@@ -53,10 +53,19 @@ struct DevCsr {
   DBuf<double> val;
 };
 
+// non-owning view of a device CSR (row-chunk slices of a DevCsr)
+struct CsrView {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int* ptr = nullptr;
+  int* idx = nullptr;
+  double* val = nullptr;
+};
+CsrView view(const DevCsr& A) { return CsrView{A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p}; }
+
 // C = A B with cuSPARSE SpGEMM.  ALG1 (the default) needs workspace that grows
 // with the intermediate products and reports INSUFFICIENT_RESOURCES on the large
 // coarse products; then ALG2 and finally the chunked ALG3 are used.
-void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
+void spgemm(cusparseHandle_t H, const CsrView& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
             const char* what) {
   CUSPARSE_CHECK(cusparseSetStream(H, s));
   const cusparseSpGEMMAlg_t algs[3] = {CUSPARSE_SPGEMM_DEFAULT, CUSPARSE_SPGEMM_ALG2,
@@ -65,7 +74,7 @@ void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cud
   for (int ai = 0; ai < 3; ++ai) {
     const cusparseSpGEMMAlg_t alg = algs[ai];
     cusparseSpMatDescr_t a, b, c;
-    CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p,
+    CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr, A.idx, A.val,
                                      CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
     CUSPARSE_CHECK(cusparseCreateCsr(&b, B.rows, B.cols, B.nnz, B.ptr.p, B.idx.p, B.val.p,
                                      CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
@@ -127,6 +136,72 @@ void spgemm(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cud
                      "x" + std::to_string(A.cols) + " nnz " + std::to_string(A.nnz) + " times " +
                      std::to_string(B.rows) + "x" + std::to_string(B.cols) + " nnz " +
                      std::to_string(B.nnz) + "):" + errs);
+}
+
+// C = A B by row chunks of A.  A chunk holds at most max_prod intermediate
+// products (sum over its entries a_ik of nnz(B row k)), which bounds cuSPARSE's
+// workspace (the single product of the c2 coarse matrix ran out of it); the
+// chunks' CSR pieces are concatenated in row order (same entries, same values
+// as the unchunked product: each output row is computed by one call).
+void spgemm_rows(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
+                 const char* what) {
+  // MDD_SPGEMM_MAX_PROD: test knob (forces chunking on small problems)
+  const int64_t max_prod = env_int("MDD_SPGEMM_MAX_PROD", 48 << 20);
+  std::vector<int> ap(A.rows + 1), bp(B.rows + 1), ai(A.nnz);
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  CUDA_CHECK(cudaMemcpy(ap.data(), A.ptr.p, ap.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaMemcpy(bp.data(), B.ptr.p, bp.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  if (A.nnz) CUDA_CHECK(cudaMemcpy(ai.data(), A.idx.p, ai.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> cut{0};
+  int64_t acc = 0;
+  for (int64_t r = 0; r < A.rows; ++r) {
+    int64_t pr = 0;
+    for (int k = ap[r]; k < ap[r + 1]; ++k) pr += bp[ai[k] + 1] - bp[ai[k]];
+    if (acc + pr > max_prod && r > cut.back()) { cut.push_back(r); acc = 0; }
+    acc += pr;
+  }
+  cut.push_back(A.rows);
+  if (cut.size() == 2) {
+    spgemm(H, view(A), B, C, s, what);
+    return;
+  }
+  std::vector<DevCsr> parts(cut.size() - 1);
+  std::vector<int64_t> pnnz(parts.size());
+  int64_t tot = 0;
+  for (size_t c = 0; c + 1 < cut.size(); ++c) {
+    const int64_t r0 = cut[c], r1 = cut[c + 1];
+    std::vector<int> rp(r1 - r0 + 1);
+    for (int64_t r = r0; r <= r1; ++r) rp[r - r0] = ap[r] - ap[r0];
+    DBuf<int> dptr;
+    dptr.upload(rp);
+    CsrView Ac{r1 - r0, A.cols, (int64_t)(ap[r1] - ap[r0]), dptr.p, A.idx.p + ap[r0], A.val.p + ap[r0]};
+    spgemm(H, Ac, B, parts[c], s, what);
+    pnnz[c] = parts[c].nnz;
+    tot += parts[c].nnz;
+  }
+  MDD_REQUIRE(tot < INT32_MAX, 5, std::string(what) + ": product too large for 32-bit CSR offsets");
+  C.rows = A.rows; C.cols = B.cols; C.nnz = tot;
+  std::vector<int> cp(A.rows + 1, 0);
+  int64_t off = 0;
+  for (size_t c = 0; c < parts.size(); ++c) {
+    std::vector<int> pp(parts[c].rows + 1);
+    CUDA_CHECK(cudaMemcpy(pp.data(), parts[c].ptr.p, pp.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < parts[c].rows; ++r) cp[cut[c] + r + 1] = (int)(off + pp[r + 1]);
+    off += pnnz[c];
+  }
+  C.ptr.upload(cp);
+  C.idx.alloc(std::max<int64_t>(tot, 1));
+  C.val.alloc(std::max<int64_t>(tot, 1));
+  off = 0;
+  for (size_t c = 0; c < parts.size(); ++c) {
+    if (pnnz[c]) {
+      CUDA_CHECK(cudaMemcpyAsync(C.idx.p + off, parts[c].idx.p, pnnz[c] * sizeof(int), cudaMemcpyDeviceToDevice, s));
+      CUDA_CHECK(cudaMemcpyAsync(C.val.p + off, parts[c].val.p, pnnz[c] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    off += pnnz[c];
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    parts[c] = DevCsr();
+  }
 }
 
 void transpose(cusparseHandle_t H, const DevCsr& A, DevCsr& T, cudaStream_t s) {
@@ -683,7 +758,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         Zit.rows = nc; Zit.cols = n; Zit.nnz = (int64_t)cdof.size();
         Zit.ptr.upload(tptr); Zit.idx.upload(tidx); Zit.val.upload(tval);
       }
-      spgemm(H->sp, Zit, Zi, G, s, "gradient Gram Zint^T Zint");
+      spgemm_rows(H->sp, Zit, Zi, G, s, "gradient Gram Zint^T Zint");
       Csr gpat;
       std::vector<int64_t> gslot;
       download_sorted(G, gpat, gslot);
@@ -785,9 +860,10 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       Ad.idx.upload(H->Apat.idx);
       Ad.val.alloc(Ad.nnz);
       CUDA_CHECK(cudaMemcpyAsync(Ad.val.p, H->A_val.p, Ad.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      spgemm(H->sp, Ad, Z, W, s, "A Z");
+      spgemm_rows(H->sp, Ad, Z, W, s, "A Z");
       transpose(H->sp, Z, Zt, s);
-      spgemm(H->sp, Zt, W, E, s, "Z^T (A Z)");
+      spgemm_rows(H->sp, Zt, W, E, s, "Z^T (A Z)");
+      W = DevCsr();
       // Jacobi scaling E <- S E S, Z <- Z S (S = diag(E)^{-1/2}): the coarse operator
       // Z E^{-1} Z^T is unchanged, the factorised matrix has a unit diagonal
       DBuf<double> sc;

@@ -83,7 +83,7 @@ struct DevFactor {
   DBuf<int32_t> gsrc;
   DBuf<double> Lt, fpart, bpart, vb;
   DBuf<unsigned long long> rb_cnt, cb_cnt, ctl, trace;
-  int nphases = 0, nphases_noprolong = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
+  int nphases = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
   // plan statistics (mdd_info): supernodes swept as packed / strip / 2-D tasks,
   // fronts factorised by the blocked (cuBLAS trailing update) path
   int n_packed = 0, n_strip = 0, n_2d = 0, n_blocked = 0;

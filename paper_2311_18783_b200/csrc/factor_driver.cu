@@ -351,7 +351,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     if (!fz) ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], fz ? 1 : 0));
   }
-  nphases_noprolong = (int)ph.size();
   if (prolong_n > 0) {
     ph.push_back(make_int4(dev::PH_PR, 0, prolong_n, 0));
     pro_ptr = pro_ptr_dev;
@@ -482,7 +481,10 @@ void DevFactor::sweep_timing(unsigned long long* ns, unsigned long long* cnt, cu
 
 void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* stop) const {
   dev::SweepDev S = sweep_dev();
-  S.nphases = out ? nphases : nphases_noprolong;
+  // the phase count must not vary between launches (the grid barrier's target is
+  // cumulative over launches): without `out` the prolongation phase runs empty
+  S.nphases = nphases;
+  S.n_out = out ? n_out : 0;
   S.b = b;
   S.out = out;
   S.stop = stop;

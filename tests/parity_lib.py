@@ -285,3 +285,67 @@ def measure_all(name):
     for v in ("as2", "as2_coarse_start"):
         out.update(measure_pcg(name, v))
     return out
+
+
+# ---------------------------------------------------------------- goldens
+GOLDEN_DIR = __import__("os").path.join(__import__("os").path.dirname(__import__("os").path.abspath(__file__)),
+                                         "golden")
+
+
+def golden_workloads():
+    """The workload recipes of tools/make_golden.py (same definitions)."""
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(GOLDEN_DIR), "..", "tools", "make_golden.py")
+    spec = importlib.util.spec_from_file_location("make_golden", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.GOLDENS
+
+
+def golden_names():
+    import os
+    return sorted(f[:-5] for f in os.listdir(GOLDEN_DIR) if f.endswith(".json")) if os.path.isdir(GOLDEN_DIR) else []
+
+
+_gcache = {}
+
+
+def golden_pair(name):
+    import json
+    import os
+    if name not in _gcache:
+        from paper_2311_18783_b200 import MaxwellDD
+        g = json.load(open(os.path.join(GOLDEN_DIR, f"{name}.json")))
+        w = golden_workloads()[name]()
+        _gcache[name] = (g, w, MaxwellDD(w))
+    return _gcache[name]
+
+
+def measure_golden(name):
+    """The device solve / preconditioner at a golden's size vs the oracle's stored
+    values (sampled entries, norms, iteration counts, integer coarse-space facts)."""
+    g, w, G = golden_pair(name)
+    out = {"n_equal": G.n == g["n"], "grad_rank_equal": int(G.info["grad_rank"]) == g["grad_rank"],
+           "geneo_counts_equal": [int(c) for c in G.int_array("geneo_count")] == g["geneo_count"],
+           "ngeneo": int(sum(g["geneo_count"]))}
+    idx = np.asarray(g["sample_idx"])
+    f = workloads.rhs(G.n, w.f_seed)
+    x = empty(G.n)
+    for variant, key, xs, xn in (("as2", "as2", "x_sample", "x_norm"),
+                                 ("as2_coarse_start", "coarse_start", "xc_sample", "xc_norm")):
+        G.set_variant(variant)
+        it, relres, ok = G.solve(dev(f), x, tol=1e-8)
+        xh = host(x)
+        out[f"{key}_iters"] = (it, g[f"iters_{key}"])
+        out[f"{key}_ok"] = bool(ok)
+        out[f"{key}_x_sample_rel"] = rel(xh[idx], np.asarray(g[xs]))
+        out[f"{key}_x_norm_rel"] = abs(np.linalg.norm(xh) - g[xn]) / g[xn]
+    G.set_variant("as2")
+    r = np.random.default_rng(g["prec_rhs_seed"]).standard_normal(G.n)
+    z = empty(G.n)
+    G.apply_preconditioner(dev(r), z)
+    zh = host(z)
+    out["prec_z_sample_rel"] = rel(zh[idx], np.asarray(g["z_sample"]))
+    out["prec_z_norm_rel"] = abs(np.linalg.norm(zh) - g["z_norm"]) / g["z_norm"]
+    return out

@@ -24,6 +24,13 @@ for name in names:
     print(name, json.dumps(res[name]), flush=True)
     with open(out + ".json", "w") as f:
         json.dump(res, f, indent=1)
+for name in PL.golden_names():
+    t0 = time.time()
+    res["golden:" + name] = PL.measure_golden(name)
+    res["golden:" + name]["seconds"] = time.time() - t0
+    print("golden", name, json.dumps(res["golden:" + name]), flush=True)
+    with open(out + ".json", "w") as f:
+        json.dump(res, f, indent=1)
 keys = ["local_vs_oracle", "local_fwd_gpu", "local_fwd_oracle", "local_bwd_gpu", "local_bwd_oracle",
         "coarse_bwd_gpu", "coarse_bwd_oracle", "coarse_vs_oracle", "coarse_fwd_gpu", "coarse_fwd_oracle",
         "prec_as2_vs_oracle", "prec_as2_fwd_gpu", "prec_as2_fwd_oracle",
@@ -33,6 +40,8 @@ with open(out + ".md", "w") as f:
     f.write("| case | " + " | ".join(keys) + " | iters gpu/oracle (as2, coarse start) |\n")
     f.write("|---" * (len(keys) + 2) + "|\n")
     for name, r in res.items():
+        if name.startswith("golden:"):
+            continue
         it = (f"{r['pcg_as2_iters_gpu']}/{r['pcg_as2_iters_oracle']}, "
               f"{r['pcg_as2_coarse_start_iters_gpu']}/{r['pcg_as2_coarse_start_iters_oracle']}")
         f.write(f"| {name} | " + " | ".join(f"{r[k]:.1e}" for k in keys) + f" | {it} |\n")
