@@ -171,6 +171,8 @@ enum {
   MDD_INFO_COARSE_SN_STRIP,
   MDD_INFO_COARSE_SN_2D,
   MDD_INFO_COARSE_BLOCKED_FRONTS,
+  MDD_INFO_GENEO_LANCZOS,   /* 1: the GenEO GEVPs were solved by block Lanczos (large
+                               subdomains), 0: dense sygvdx per subdomain           */
   MDD_INFO_COUNT
 };
 int mdd_info(mdd_handle h, int64_t* out, int count);

@@ -24,7 +24,8 @@ INFO_NAMES = ["n", "nedges", "nfree_nodes", "nsub", "nnz_A", "nloc", "grad_candi
               "nnz_Z", "kernels_per_iter", "last_launches",
               "coarse_perturbed", "nnz_Zg", "nnz_W",
               "local_sn_packed", "local_sn_strip", "local_sn_2d", "local_blocked_fronts",
-              "coarse_sn_packed", "coarse_sn_strip", "coarse_sn_2d", "coarse_blocked_fronts"]
+              "coarse_sn_packed", "coarse_sn_strip", "coarse_sn_2d", "coarse_blocked_fronts",
+              "geneo_lanczos"]
 INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, "A_ptr": 4,
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
               "geneo_count": 10, "E_ptr": 11, "E_idx": 12}

@@ -285,6 +285,7 @@ struct mdd_solver {
   int64_t n0 = 0, grad_cand = 0, grad_rank = 0, ngeneo = 0, nnzZ = 0, coarse_perturbed = 0;
   std::vector<int64_t> geneo_count;
   std::vector<double> geneo_lambda;
+  bool geneo_lanczos = false;   // GenEO GEVPs by block Lanczos (else dense sygvdx)
   // parity diagnostics: the factorised (Jacobi-scaled) E in its original column
   // order (sorted pattern + value slots into E_val) and, per subdomain-major local
   // dof (sys_off[i] + k, k in N_i order), its position in the local factor
@@ -661,8 +662,17 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     std::vector<GeneoBlock> geneo(nsub);
     if (d->coarse_threshold > 0) {
       const double tau = 1.0 / d->coarse_threshold;
-      GeneoInputs gin{&m, &H->dec, &lpat, &lslot, H->A_val.p, H->Ke.p, H->Me.p, d->gamma, &H->grad_nodes};
-      geneo_all(gin, tau, geneo, s);
+      GeneoInputs gin{&m, &H->dec, &lpat, &lslot, H->A_val.p, H->Ke.p, H->Me.p, d->gamma, &H->grad_nodes, &lxyz};
+      // dense sygvdx per subdomain up to MDD_GENEO_DENSE_MAX local dofs, block
+      // Lanczos over all subdomains above (MDD_GENEO=dense|lanczos forces a path)
+      size_t nmax = 0;
+      for (int i = 0; i < nsub; ++i) nmax = std::max(nmax, H->dec.sub_dofs[i].size());
+      const char* gsel = getenv("MDD_GENEO");
+      const bool lanczos = gsel ? std::string(gsel) == "lanczos"
+                                : nmax > (size_t)env_int("MDD_GENEO_DENSE_MAX", 12000);
+      H->geneo_lanczos = lanczos;
+      if (lanczos) geneo_lanczos(gin, tau, geneo, s);
+      else geneo_all(gin, tau, geneo, s);
       for (int i = 0; i < nsub; ++i) {
         H->geneo_count[i] = geneo[i].k;
         for (double l : geneo[i].lambda) H->geneo_lambda.push_back(l);
@@ -1347,6 +1357,7 @@ int mdd_info(mdd_handle h, int64_t* out, int count) {
   v[MDD_INFO_COARSE_SN_STRIP] = h->has_coarse ? h->crs.n_strip : 0;
   v[MDD_INFO_COARSE_SN_2D] = h->has_coarse ? h->crs.n_2d : 0;
   v[MDD_INFO_COARSE_BLOCKED_FRONTS] = h->has_coarse ? h->crs.n_blocked : 0;
+  v[MDD_INFO_GENEO_LANCZOS] = h->geneo_lanczos ? 1 : 0;
   v[MDD_INFO_LAST_LAUNCHES] = h->launches;
   v[MDD_INFO_COARSE_PERTURBED] = h->coarse_perturbed;
   v[MDD_INFO_NNZ_ZG] = h->nnzZg;

@@ -28,6 +28,49 @@ namespace mdd {
 
 static inline int nb(int64_t n, int t) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
 
+void neumann_slots(const HostMesh& m, const Decomp& dec, const Csr& lp, int j, std::vector<int32_t>& g2l,
+                   std::vector<int64_t>& cnt, std::vector<int32_t>& ctb) {
+  const auto& D = dec.sub_dofs[j];
+  for (size_t k = 0; k < D.size(); ++k) g2l[D[k]] = (int32_t)k;
+  cnt.assign(lp.nnz() + 1, 0);
+  std::vector<std::pair<int64_t, int32_t>> cl;  // (slot, contrib)
+  for (int32_t t : dec.sub_tets[j])
+    for (int a = 0; a < 6; ++a) {
+      int ea = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + a]];
+      if (ea < 0) continue;
+      int la = g2l[ea];
+      for (int b = 0; b < 6; ++b) {
+        int eb = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + b]];
+        if (eb < 0) continue;
+        int lb = g2l[eb];
+        const int32_t* b0 = lp.idx.data() + lp.ptr[la];
+        const int32_t* b1 = lp.idx.data() + lp.ptr[la + 1];
+        int64_t slot = (int64_t)(std::lower_bound(b0, b1, lb) - lp.idx.data());
+        cl.push_back({slot, (int32_t)((int64_t)t * 36 + a * 6 + b)});
+      }
+    }
+  std::stable_sort(cl.begin(), cl.end(), [](const std::pair<int64_t, int32_t>& x,
+                                             const std::pair<int64_t, int32_t>& y) { return x.first < y.first; });
+  ctb.resize(cl.size());
+  for (size_t q = 0; q < cl.size(); ++q) { cnt[cl[q].first + 1]++; ctb[q] = cl[q].second; }
+  for (int64_t q = 0; q < lp.nnz(); ++q) cnt[q + 1] += cnt[q];
+  for (size_t k = 0; k < D.size(); ++k) g2l[D[k]] = -1;
+}
+
+void gradient_entries(const HostMesh& m, const std::vector<int32_t>& D, const std::vector<int32_t>& gn,
+                      std::vector<int32_t>& colof, std::vector<int32_t>& row, std::vector<int32_t>& col,
+                      std::vector<double>& val) {
+  row.clear(); col.clear(); val.clear();
+  for (size_t c = 0; c < gn.size(); ++c) colof[gn[c]] = (int32_t)c;
+  for (size_t k = 0; k < D.size(); ++k) {
+    int ee = m.free_edge[D[k]];
+    int a = m.node_to_free[m.edge_tail[ee]], b = m.node_to_free[m.edge_head[ee]];
+    if (a >= 0 && colof[a] >= 0) { row.push_back((int32_t)k); col.push_back(colof[a]); val.push_back(-1.0); }
+    if (b >= 0 && colof[b] >= 0) { row.push_back((int32_t)k); col.push_back(colof[b]); val.push_back(1.0); }
+  }
+  for (size_t c = 0; c < gn.size(); ++c) colof[gn[c]] = -1;
+}
+
 
 void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, cudaStream_t s) {
   const HostMesh& m = *in.mesh;
@@ -42,6 +85,7 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
   CUBLAS_CHECK(cublasSetStream(cb, s));
   CUSOLVER_CHECK(cusolverDnSetStream(cs, s));
   std::vector<int32_t> g2l(m.n(), -1);
+  std::vector<int32_t> colof(m.free_node.size() ? m.free_node.size() : 1, -1);
   DBuf<int> info;
   info.alloc(1);
   try {
@@ -50,52 +94,26 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
       const int64_t n = (int64_t)D.size();
       const Csr& lp = (*in.lpat)[j];
       const auto& ls = (*in.lslot)[j];
-      for (int64_t k = 0; k < n; ++k) g2l[D[k]] = (int32_t)k;
       // dense positions of the local pattern
       std::vector<int64_t> dpos(lp.nnz());
       for (int64_t r = 0; r < n; ++r)
         for (int64_t p = lp.ptr[r]; p < lp.ptr[r + 1]; ++p) dpos[p] = (int64_t)lp.idx[p] * n + r;
       // Neumann contributions per local slot from the tets of Omega_j (fixed order)
-      std::vector<int64_t> cnt(lp.nnz() + 1, 0);
-      std::vector<std::pair<int64_t, int32_t>> cl;  // (slot, contrib)
-      for (int32_t t : dec.sub_tets[j])
-        for (int a = 0; a < 6; ++a) {
-          int ea = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + a]];
-          if (ea < 0) continue;
-          int la = g2l[ea];
-          for (int b = 0; b < 6; ++b) {
-            int eb = m.edge_to_free[m.tet_edge[(int64_t)t * 6 + b]];
-            if (eb < 0) continue;
-            int lb = g2l[eb];
-            const int32_t* b0 = lp.idx.data() + lp.ptr[la];
-            const int32_t* b1 = lp.idx.data() + lp.ptr[la + 1];
-            int64_t slot = (int64_t)(std::lower_bound(b0, b1, lb) - lp.idx.data());
-            cl.push_back({slot, (int32_t)((int64_t)t * 36 + a * 6 + b)});
-          }
-        }
-      std::stable_sort(cl.begin(), cl.end(), [](const std::pair<int64_t, int32_t>& x,
-                                                 const std::pair<int64_t, int32_t>& y) { return x.first < y.first; });
-      std::vector<int32_t> ctb(cl.size());
-      for (size_t q = 0; q < cl.size(); ++q) { cnt[cl[q].first + 1]++; ctb[q] = cl[q].second; }
-      for (int64_t q = 0; q < lp.nnz(); ++q) cnt[q + 1] += cnt[q];
+      std::vector<int64_t> cnt;
+      std::vector<int32_t> ctb;
+      neumann_slots(m, dec, lp, j, g2l, cnt, ctb);
       // gradient columns
       const auto& gn = (*in.grad_nodes)[j];
       const int64_t g = (int64_t)gn.size();
       std::vector<int64_t> gpos;
       std::vector<double> gval;
       {
-        std::vector<int32_t> colof(m.free_node.size() ? m.free_node.size() : 1, -1);
-        for (int64_t c = 0; c < g; ++c) colof[gn[c]] = (int32_t)c;
-        for (int64_t k = 0; k < n; ++k) {
-          int ee = m.free_edge[D[k]];
-          int a = m.node_to_free[m.edge_tail[ee]], b = m.node_to_free[m.edge_head[ee]];
-          if (a >= 0 && colof[a] >= 0) { gpos.push_back((int64_t)colof[a] * n + k); gval.push_back(-1.0); }
-          if (b >= 0 && colof[b] >= 0) { gpos.push_back((int64_t)colof[b] * n + k); gval.push_back(1.0); }
-        }
+        std::vector<int32_t> grow, gcol;
+        gradient_entries(m, D, gn, colof, grow, gcol, gval);
+        for (size_t q = 0; q < grow.size(); ++q) gpos.push_back((int64_t)gcol[q] * n + grow[q]);
       }
       std::vector<double> Dw(n);
       for (int64_t k = 0; k < n; ++k) Dw[k] = 1.0 / (double)dec.mult[D[k]];
-      for (int64_t k = 0; k < n; ++k) g2l[D[k]] = -1;
 
       // ---- device work
       DBuf<double> Ad, Bd, P, T1, G, W1, Sg, Xt, dw, vals, lam;
