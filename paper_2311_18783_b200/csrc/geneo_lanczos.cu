@@ -22,7 +22,8 @@
 // Dense b x b / m x b pieces are strided-batched cuBLAS; the block-tridiagonal T is
 // diagonalised by cuSOLVER syevd at a few checkpoints, where the host reads only
 // the Ritz values and the residual bounds ||R_k s_i(last block)|| to decide
-// convergence (a Ritz pair is converged at residual <= 1e-10 max(theta_max, 1);
+// convergence (a Ritz pair is converged at residual <= 1e-10 max(theta, tau),
+// floored at 1e-14 theta_max;
 // a subdomain is done when every Ritz value above tau and the largest one below
 // it are converged and the count above tau did not change since the previous
 // checkpoint).
@@ -508,7 +509,11 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
           for (int c = a; c < b; ++c) t += R[c * b + a] * last[(size_t)i * b + c];
           r2 += t * t;
         }
-        if (std::sqrt(r2) > rtol * tmax) conv = false;
+        // Ritz value error <= residual: relative to the eigenvalue itself (the kept
+        // ones span many decades on high-contrast recipes), floored at what fp64
+        // Lanczos can reach (~eps * theta_max)
+        const double lim = std::max(rtol * std::max(std::fabs(wj[i]), tau), 1e-14 * tmax);
+        if (std::sqrt(r2) > lim) conv = false;
         if (wj[i] <= tau) break;  // the largest Ritz value below tau was checked too
       }
       if (conv && cnt == prev_cnt[j]) {

@@ -366,6 +366,11 @@ def measure_golden(name):
         out[f"{key}_ok"] = bool(ok)
         out[f"{key}_x_sample_rel"] = rel(xh[idx], np.asarray(g[xs]))
         out[f"{key}_x_norm_rel"] = abs(np.linalg.norm(xh) - g[xn]) / g[xn]
+        if variant == "as2":
+            from oracle import assembly, mesh as om
+            A, _, _ = assembly.system_matrix(om.mesh_of(w), w.mu_inv, w.eps, w.gamma)
+            out["as2_true_res"] = (float(np.linalg.norm(f - A @ xh) / np.linalg.norm(f)), g["true_res_as2"])
+            out["as2_backward_error"] = backward_error(A.tocsr(), xh, f)
     G.set_variant("as2")
     r = np.random.default_rng(g["prec_rhs_seed"]).standard_normal(G.n)
     z = empty(G.n)

@@ -1,8 +1,11 @@
-"""GPU checks at BASELINE's full c1 size (the configuration bench.py times), where
-the oracle cannot run end to end: sampled outputs the oracle computes one by one
-(a single subdomain's local solve, the true residual with the oracle's own A) and
-properties that hold at any size (P0 = QA is an A-orthogonal projection, M
-symmetric)."""
+"""GPU checks at BASELINE's full c1 size, where the oracle cannot run end to end
+(its SNK basis needs a dense eigendecomposition of the 64k-column candidate
+Gram): kappa-free backward errors of every subdomain solve, of the coarse solve
+and of the PCG solution against the oracle's own A; forward errors of sampled
+subdomain solves against the extended-precision reference; properties that hold
+at any size (P0 = QA is an A-orthogonal projection, M symmetric).  The oracle's
+own answers at the bench's 4^3 partition come from the 16^3 goldens
+(tests/test_gpu_golden.py)."""
 import numpy as np
 import pytest
 import scipy.sparse.linalg as spla
@@ -35,33 +38,51 @@ def test_assembled_matrix_full_size(c1):
     assert np.abs(G.double_array("A_val") - A.data).max() <= 1e-13 * np.abs(A.data).max()
 
 
-@pytest.mark.parametrize("sub", [0, 21, 63])
-def test_single_subdomain_local_solve(c1, sub):
-    # r supported on dofs that only subdomain `sub` owns (multiplicity 1) has
-    # R_j r = 0 for j != sub, so M_AS r = R_sub^T A_sub^{-1} R_sub r (eq. AS)
+def test_every_local_solve_is_backward_stable_full_size(c1):
+    """All 64 subdomain solves A_i x_i = R_i r of the full-size c1 (the bench's
+    configuration), through mdd_apply_local_parts: normwise backward error at most
+    8 eps on every subdomain (kappa-free: kappa(A_i) ~ 1e11 here), and on three
+    subdomains the forward error against the extended-precision reference is at
+    most 4x that of the oracle's own fp64 direct solver (SuperLU)."""
+    from oracle import refine
+    from parity_lib import EPS, backward_error, rel_ld
     w, G, A, dec = c1
-    d = dec.dofs[sub]
-    own = d[dec.mult[d] == 1]
-    rng = np.random.default_rng(sub)
-    r = np.zeros(A.shape[0])
-    r[own] = rng.standard_normal(len(own))
-    z = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
-    G.apply_local(dev(r), z)
-    Ai = A[d][:, d].tocsc()
-    zi = spla.splu(Ai).solve(r[d])
-    ref = np.zeros_like(r)
-    ref[d] = zi
-    zg = z.cpu().numpy()
-    # kappa(A_i) ~ 1e11 for the contrast-1e4, gamma-1e-4 recipe (R9)
-    assert np.linalg.norm(zg - ref) <= 1e-4 * np.linalg.norm(ref)
-    # backward stability: the residual is at the level of a direct solver's
-    # (||A_i|| ||z|| eps), here compared with SuperLU's own residual
-    res = np.linalg.norm(Ai @ zg[d] - r[d])
-    res_lu = np.linalg.norm(Ai @ zi - r[d])
-    bound = np.finfo(float).eps * spla.norm(Ai, 1) * np.linalg.norm(zi)
-    assert res <= 100 * max(res_lu, bound)
-    outside = np.setdiff1d(np.arange(len(r)), d)
-    assert not zg[outside].any()
+    r = np.random.default_rng(11).standard_normal(A.shape[0])
+    xl = torch.empty(int(G.info["nloc"]), dtype=torch.float64, device="cuda")
+    G.apply_local_parts(dev(r), xl)
+    xl = xl.cpu().numpy()
+    sp_ = G.int_array("sub_ptr")
+    worst = 0.0
+    for i, d in enumerate(dec.dofs):
+        assert np.array_equal(G.int_array("sub_dofs")[sp_[i]:sp_[i + 1]], d)
+        Ai = A[d][:, d].tocsr()
+        worst = max(worst, backward_error(Ai, xl[sp_[i]:sp_[i + 1]], r[d]))
+    assert worst <= 8 * EPS, worst
+    for i in (0, 21, 63):
+        d = dec.dofs[i]
+        Ai = A[d][:, d].tocsr()
+        lu = spla.splu(Ai.tocsc())
+        xr = refine.refined_solve(Ai, r[d], lu)
+        e_gpu = rel_ld(xl[sp_[i]:sp_[i + 1]], xr)
+        e_lu = rel_ld(lu.solve(r[d]), xr)
+        assert e_gpu <= 4 * max(e_lu, EPS), (i, e_gpu, e_lu)
+
+
+def test_coarse_solve_backward_error_full_size(c1):
+    """E y = v on the full-size c1 coarse matrix (n0 ~ 51k, kappa ~ 1e13): the
+    normwise backward error of the device's static-pivot supernodal LDL^T with
+    partitioned-inverse panels, at 10x the observation on the same machine
+    (it is larger than a dense Cholesky's, ~1e-12 vs 1e-17)."""
+    from parity_lib import backward_error
+    w, G, A, dec = c1
+    n0 = int(G.info["n0"])
+    E = G.coarse_matrix()
+    v = np.random.default_rng(12).standard_normal(n0)
+    y = torch.empty(n0, dtype=torch.float64, device="cuda")
+    G.apply_coarse_inverse(dev(v), y)
+    be = backward_error(E, y.cpu().numpy(), v)
+    print(f"c1 full-size coarse backward error {be:.2e}")
+    assert be <= 1e-11, be
 
 
 def test_coarse_projection_properties(c1):
@@ -84,14 +105,21 @@ def test_coarse_projection_properties(c1):
 
 
 def test_pcg_full_size(c1):
+    """Full-size c1 PCG: converged, bit-reproducible, and the solution's normwise
+    backward error ||f - A x|| / (||A|| ||x|| + ||f||) (kappa-free) is below
+    1e-12: the iterate solves a nearby system, whatever kappa(A) ~ 1e11 does to
+    its forward error; the true relative residual is reported beside it."""
+    from parity_lib import backward_error
     w, G, A, dec = c1
     f = workloads.rhs(A.shape[0], w.f_seed)
     x = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
     it, rel, ok = G.solve(dev(f), x, tol=1e-8)
     assert ok and rel <= 1e-8 and 10 <= it <= 200
     xh = x.cpu().numpy()
-    # true residual with the oracle's A: CG's attainable accuracy at kappa(A) ~ 1e11
-    assert np.linalg.norm(f - A @ xh) <= 1e-3 * np.linalg.norm(f)
+    be = backward_error(A, xh, f)
+    tr = np.linalg.norm(f - A @ xh) / np.linalg.norm(f)
+    print(f"c1 full size: {it} iterations, backward error {be:.2e}, true relative residual {tr:.2e}")
+    assert be <= 1e-12, be
     it2, rel2, ok2 = G.solve(dev(f), x, tol=1e-8)
     assert it2 == it and np.array_equal(x.cpu().numpy(), xh)   # bit-reproducible
 
@@ -114,7 +142,10 @@ def test_pcg_full_size_coarse_start(c1):
     finally:
         G.set_variant("as2")
     assert ok and rel <= 1e-8 and abs(it - it0) <= 1
-    assert np.linalg.norm(f - A @ xh) <= 1e-3 * np.linalg.norm(f)
+    from parity_lib import backward_error
+    assert backward_error(A, xh, f) <= 1e-12
+    # the two loops' solutions differ by the fp64 solvers' own accuracy at kappa ~ 1e11
+    # (the golden runs at 16^3 show 5e-6 between device and oracle)
     assert np.linalg.norm(xh - x0) <= 1e-4 * np.linalg.norm(x0)
 
 

@@ -24,9 +24,31 @@ def test_row_chunked_spgemm_gives_the_same_coarse_matrix():
     finally:
         os.environ.pop("MDD_SPGEMM_MAX_PROD", None)
     E0, E1 = G0.coarse_matrix(), G1.coarse_matrix()
-    assert np.array_equal(E0.indptr, E1.indptr) and np.array_equal(E0.indices, E1.indices)
-    assert np.abs(E0.data - E1.data).max() <= 1e-14 * np.abs(E0.data).max()
+    # (cuSPARSE may keep a structurally present but cancelled entry in one product
+    # and not in the other: compare the matrices, not their stored patterns)
+    assert abs(E0 - E1).max() <= 1e-14 * abs(E0).max()
     f = workloads.rhs(G0.n, w.f_seed)
     x0, it0, _ = G0.solve_host(f)
     x1, it1, _ = G1.solve_host(f)
     assert it0 == it1 and np.linalg.norm(x0 - x1) <= 1e-8 * np.linalg.norm(x0)
+
+
+@pytest.mark.parametrize("name", ["c1-lit-8", "c4-lit-12", "c1-recipe-8", "holes-8", "c3-recipe-12",
+                                  "c4-recipe-12", "c4-recipe-x2"])
+def test_block_lanczos_geneo_matches_the_oracle(name):
+    """The block-Lanczos GEVP path (what c3 / c4 subdomains take) forced on the
+    parity cases: GenEO counts bit-exact, eigenvalues at 1e-8 on the literal
+    cases (10x the dense path's observed difference on the ill-conditioned ones),
+    the preconditioner at north_star's 1e-10 (literal) / 10x the observation, and
+    the same PCG iteration count."""
+    from parity_lib import CASES_LITERAL, measure_lanczos
+    from parity_observed import OBSERVED
+    m = measure_lanczos(name)
+    assert m["lz_used"] == 1 and m["lz_counts_equal"], m
+    it, ito, ok = m["lz_pcg_iters"]
+    assert ok and abs(it - ito) <= 1, m
+    if name in CASES_LITERAL:
+        assert m["lz_lambda_rel"] <= 1e-8 and m["lz_prec_vs_oracle"] <= 1e-10, m
+    else:
+        assert m["lz_lambda_rel"] <= max(10 * OBSERVED[name]["geneo_lambda_rel"], 1e-8), m
+        assert m["lz_prec_vs_oracle"] <= 10 * OBSERVED[name]["prec_as2_fwd_gpu"] + 10 * OBSERVED[name]["local_fwd_gpu"], m
