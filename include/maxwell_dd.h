@@ -205,6 +205,24 @@ int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_
 int mdd_topology_int_array(const mdd_setup_desc* desc, int which, int64_t* out, int64_t cap,
                            int64_t* len);
 
+/* Host-only plan of the sharded solve (no device needed): for `rank` of `nranks`
+ * ranks, the rank's subdomains (slabs along x), owned dofs, halo dofs and the
+ * per-peer exchange lists in the rank's local numbering (owned dofs first, then
+ * the halo), plus every dof's owner.  Arrays as for mdd_get_int_array. */
+enum {
+  MDD_SHARD_SUBS = 0,       /* this rank's subdomains (ascending)                       */
+  MDD_SHARD_OWNED,          /* global dofs owned (ascending) = local 0 .. n_own-1       */
+  MDD_SHARD_HALO,           /* global dofs read from other ranks = local n_own ..       */
+  MDD_SHARD_SEND_PTR,       /* nranks+1 offsets into MDD_SHARD_SEND_IDX                 */
+  MDD_SHARD_SEND_IDX,       /* per peer: local indices of owned dofs in its halo        */
+  MDD_SHARD_RECV_PTR,       /* nranks+1 offsets into MDD_SHARD_RECV_IDX                 */
+  MDD_SHARD_RECV_IDX,       /* per peer: local indices of halo dofs it owns             */
+  MDD_SHARD_DOF_OWNER,      /* per global dof: owning rank                              */
+  MDD_SHARD_COUNT
+};
+int mdd_shard_int_array(const mdd_setup_desc* desc, int rank, int nranks, int which, int64_t* out,
+                        int64_t cap, int64_t* len);
+
 /* Copy an internal double array to HOST memory. */
 enum {
   MDD_DARR_A_VAL = 0,       /* values of A in MDD_ARR_A_IDX order         */

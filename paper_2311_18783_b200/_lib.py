@@ -30,6 +30,8 @@ INT_ARRAYS = {"edge_tail": 0, "edge_head": 1, "free_edges": 2, "free_nodes": 3, 
               "A_idx": 5, "sub_ptr": 6, "sub_dofs": 7, "grad_nodes_ptr": 8, "grad_nodes": 9,
               "geneo_count": 10, "E_ptr": 11, "E_idx": 12}
 DBL_ARRAYS = {"A_val": 0, "K_val": 1, "M_val": 2, "geneo_lambda": 3, "setup_times": 4, "E_val": 5}
+SHARD_ARRAYS = {"subs": 0, "owned": 1, "halo": 2, "send_ptr": 3, "send_idx": 4, "recv_ptr": 5, "recv_idx": 6,
+                "dof_owner": 7}
 PROF_NAMES = ["spmv", "local", "prec_other", "coarse", "vector", "total"]
 
 
@@ -47,7 +49,7 @@ EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_s
            "mdd_apply_preconditioner",
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_apply_local_parts",
            "mdd_apply_coarse_inverse", "mdd_info",
-           "mdd_get_int_array", "mdd_topology_int_array", "mdd_get_double_array",
+           "mdd_get_int_array", "mdd_topology_int_array", "mdd_shard_int_array", "mdd_get_double_array",
            "mdd_phase_name", "mdd_set_profiling", "mdd_sweep_timing", "mdd_profile", "mdd_last_error"]
 
 
@@ -75,6 +77,7 @@ def load() -> C.CDLL:
         "mdd_info": (C.c_int, [P, lp, C.c_int]),
         "mdd_get_int_array": (C.c_int, [P, C.c_int, lp, C.c_int64, lp]),
         "mdd_topology_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, lp, C.c_int64, lp]),
+        "mdd_shard_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, C.c_int, C.c_int, lp, C.c_int64, lp]),
         "mdd_get_double_array": (C.c_int, [P, C.c_int, dp, C.c_int64, lp]),
         "mdd_phase_name": (C.c_char_p, [C.c_int]),
         "mdd_set_profiling": (C.c_int, [P, C.c_int]),

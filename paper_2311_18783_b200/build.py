@@ -12,7 +12,7 @@ LIB = os.environ.get("MDD_LIB_PATH") or os.path.join(HERE, "libmaxwell_dd.so")
 EXTRA = os.environ.get("MDD_NVCC_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
+SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "shard.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
            "geneo.cu", "geneo_lanczos.cu", "api.cu"]
 
 

@@ -19,6 +19,7 @@
 #include "../../include/maxwell_dd.h"
 #include "device.h"
 #include "geneo.h"
+#include "shard.h"
 #include "topology.h"
 
 using namespace mdd;
@@ -1415,6 +1416,37 @@ void coarse_matrix_pos(mdd_handle h, std::vector<int64_t>* ptr, std::vector<int6
   if (val) *val = std::move(vv);
 }
 }  // namespace
+
+int mdd_shard_int_array(const mdd_setup_desc* d, int rank, int nranks, int which, int64_t* out, int64_t cap,
+                        int64_t* len) {
+  if (!d || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    HostMesh mesh;
+    build_mesh(mesh, d->nx, d->ny, d->nz, d->h, d->cube_mask, d->dirichlet);
+    Csr Apat;
+    std::vector<int64_t> sp_;
+    std::vector<int32_t> ct;
+    build_A_pattern(mesh, Apat, sp_, ct);
+    Decomp dec;
+    build_subdomains(mesh, d->px, d->py, d->pz, d->overlap, dec);
+    ShardPlan P;
+    build_shard_plan(mesh, dec, Apat, d->px, d->py, d->pz, rank, nranks, P);
+    std::vector<int64_t> v;
+    switch (which) {
+      case MDD_SHARD_SUBS: v.assign(P.subs.begin(), P.subs.end()); break;
+      case MDD_SHARD_OWNED: v.assign(P.owned.begin(), P.owned.end()); break;
+      case MDD_SHARD_HALO: v.assign(P.halo.begin(), P.halo.end()); break;
+      case MDD_SHARD_SEND_PTR: v = P.send_ptr; break;
+      case MDD_SHARD_SEND_IDX: v.assign(P.send_idx.begin(), P.send_idx.end()); break;
+      case MDD_SHARD_RECV_PTR: v = P.recv_ptr; break;
+      case MDD_SHARD_RECV_IDX: v.assign(P.recv_idx.begin(), P.recv_idx.end()); break;
+      case MDD_SHARD_DOF_OWNER: v.assign(P.dof_owner.begin(), P.dof_owner.end()); break;
+      default: throw Error(MDD_ERR_ARG, "unknown shard array");
+    }
+    *len = (int64_t)v.size();
+    if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, *len), out);
+  });
+}
 
 int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len) {
   if (!h || !len) { g_err = "null argument"; return MDD_ERR_ARG; }

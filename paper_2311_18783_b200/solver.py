@@ -40,6 +40,18 @@ def topology_array(w, name: str) -> np.ndarray:
     return out
 
 
+def shard_array(w, rank: int, nranks: int, name: str) -> np.ndarray:
+    """Host-only sharded-solve plan of `rank` (mdd_shard_int_array)."""
+    d, keep = _desc(w)
+    n = C.c_int64(0)
+    which = L.SHARD_ARRAYS[name]
+    L.check(L.lib().mdd_shard_int_array(C.byref(d), rank, nranks, which, None, 0, C.byref(n)))
+    out = np.empty(n.value, np.int64)
+    L.check(L.lib().mdd_shard_int_array(C.byref(d), rank, nranks, which,
+                                        out.ctypes.data_as(C.POINTER(C.c_int64)), n.value, C.byref(n)))
+    return out
+
+
 def _ptr(t, n=None, device=None) -> int:
     """Device pointer of a contiguous float64 CUDA tensor of n elements on the
     handle's device (the C ABI reads / writes exactly n doubles)."""
