@@ -156,8 +156,9 @@ enum {
   MDD_INFO_NNZ_Z,
   MDD_INFO_KERNELS_PER_ITER, /* kernel launches per PCG iteration       */
   MDD_INFO_LAST_LAUNCHES,   /* kernels launched by the last solve/apply call */
-  MDD_INFO_COARSE_PERTURBED,/* pivots of the Jacobi-scaled E raised to the static-pivot
-                               threshold 1e-14 (kappa(E) ~ 1/eps; 0 = exact LDL^T)   */
+  MDD_INFO_COARSE_PERTURBED,/* pivots of the Jacobi-scaled E at or below 1e-14: numerically
+                               dependent coarse directions, dropped (D^{-1} = 0); 0 =
+                               exact LDL^T (reading R11)                    */
   MDD_INFO_NNZ_ZG,          /* entries of the gradient (SNK / NK) part of Z        */
   MDD_INFO_NNZ_W,           /* entries of the dense GenEO blocks of Z              */
   /* plan statistics: supernodes swept as packed small tasks / strips / 2-D tile
@@ -222,6 +223,33 @@ enum {
 };
 int mdd_shard_int_array(const mdd_setup_desc* desc, int rank, int nranks, int which, int64_t* out,
                         int64_t cap, int64_t* len);
+
+/* Sharded solve.  After mdd_setup of the whole problem on every
+ * rank (the setup is replicated), mdd_shard_setup(h, rank, nranks) builds this
+ * rank's hot-path data: its owned rows of A, the supernodal factor of its
+ * subdomains (prolongation onto its owned + halo dofs), its owned rows of Z and
+ * the halo exchange lists of mdd_shard_int_array.  The PCG vectors of a rank
+ * are its owned dofs (MDD_SHARD_OWNED order, n_own of mdd_shard_info).  Only
+ * MDD_VARIANT_AS2_COARSE_START (the coarse correction z = w + Q(r - A w) with
+ * one n0-allreduce per iteration; E^{-1} is applied by every rank) and
+ * MDD_VARIANT_AS1 are sharded.
+ * mdd_shard_info: out[0] n_own, [1] n_own + halo, [2] subdomains, [3] their
+ *   factor entries.
+ * mdd_shard_nccl_init: NCCL communicator of the ranks (unique_id: the 128-byte
+ *   ncclUniqueId of rank 0, broadcast by the caller, e.g. torch.distributed).
+ * mdd_shard_solve: one rank's part of the sharded PCG; f_own / x_own: n_own
+ *   doubles, DEVICE pointers (host = 0) or HOST pointers (host = 1, copies
+ *   inside); every rank calls it collectively.
+ * mdd_shard_solve_group: `count` handles of ONE process on one device, handle k
+ *   set up as rank k of count, exchanging through device copies (DEVICE
+ *   pointers); the sequence of kernels is the NCCL path's, rank by rank. */
+int mdd_shard_setup(mdd_handle h, int rank, int nranks);
+int mdd_shard_info(mdd_handle h, int64_t* out, int count);
+int mdd_shard_nccl_init(mdd_handle h, const void* unique_id, int rank, int nranks);
+int mdd_shard_solve(mdd_handle h, const double* f_own, double* x_own, double tol, int maxit, int host,
+                    int* iters, double* relres);
+int mdd_shard_solve_group(mdd_handle* hs, int count, const double* const* f_own, double* const* x_own,
+                          double tol, int maxit, int* iters, double* relres);
 
 /* Copy an internal double array to HOST memory. */
 enum {

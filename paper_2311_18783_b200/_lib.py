@@ -48,7 +48,8 @@ class SetupDesc(C.Structure):
 EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_stream", "mdd_set_variant",
            "mdd_apply_preconditioner",
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_apply_local_parts",
-           "mdd_apply_coarse_inverse", "mdd_info",
+           "mdd_apply_coarse_inverse", "mdd_shard_setup", "mdd_shard_info", "mdd_shard_nccl_init",
+           "mdd_shard_solve", "mdd_shard_solve_group", "mdd_info",
            "mdd_get_int_array", "mdd_topology_int_array", "mdd_shard_int_array", "mdd_get_double_array",
            "mdd_phase_name", "mdd_set_profiling", "mdd_sweep_timing", "mdd_profile", "mdd_last_error"]
 
@@ -74,6 +75,12 @@ def load() -> C.CDLL:
         "mdd_apply_coarse": (C.c_int, [P, P, P]),
         "mdd_apply_local_parts": (C.c_int, [P, P, P]),
         "mdd_apply_coarse_inverse": (C.c_int, [P, P, P]),
+        "mdd_shard_setup": (C.c_int, [P, C.c_int, C.c_int]),
+        "mdd_shard_info": (C.c_int, [P, lp, C.c_int]),
+        "mdd_shard_nccl_init": (C.c_int, [P, C.c_char_p, C.c_int, C.c_int]),
+        "mdd_shard_solve": (C.c_int, [P, P, P, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int), dp]),
+        "mdd_shard_solve_group": (C.c_int, [C.POINTER(P), C.c_int, C.POINTER(P), C.POINTER(P), C.c_double,
+                                            C.c_int, C.POINTER(C.c_int), dp]),
         "mdd_info": (C.c_int, [P, lp, C.c_int]),
         "mdd_get_int_array": (C.c_int, [P, C.c_int, lp, C.c_int64, lp]),
         "mdd_topology_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, lp, C.c_int64, lp]),

@@ -13,7 +13,7 @@ EXTRA = os.environ.get("MDD_NVCC_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "shard.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
-           "geneo.cu", "geneo_lanczos.cu", "api.cu"]
+           "geneo.cu", "geneo_lanczos.cu", "api.cu", "sharded.cu"]
 
 
 def _newer(target, deps):
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed")
     cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcusparse", "-lcublas", "-lcusolver",
-           "-lcudart"]
+           "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)
     return LIB
 

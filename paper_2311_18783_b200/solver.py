@@ -230,6 +230,33 @@ class MaxwellDD:
         return sp.csr_matrix((self.double_array("E_val"), self.int_array("E_idx"), self.int_array("E_ptr")),
                              shape=(n0, n0))
 
+    # ------------------------------------------------------ sharded solve
+    def shard_setup(self, rank: int, nranks: int):
+        """This handle becomes rank `rank` of a sharded solve (mdd_shard_setup)."""
+        L.check(L.lib().mdd_shard_setup(self._h, rank, nranks))
+        out = (C.c_int64 * 4)()
+        L.check(L.lib().mdd_shard_info(self._h, out, 4))
+        self.shard = {"rank": rank, "nranks": nranks, "n_own": int(out[0]), "n_local": int(out[1]),
+                      "subdomains": int(out[2]), "factor_nnz": int(out[3])}
+        self.owned = shard_array(self.w, rank, nranks, "owned")
+        return self.shard
+
+    def shard_nccl_init(self, unique_id: bytes):
+        """NCCL communicator of the ranks (unique_id: 128 bytes from rank 0)."""
+        L.check(L.lib().mdd_shard_nccl_init(self._h, bytes(unique_id), self.shard["rank"], self.shard["nranks"]))
+
+    def shard_solve(self, f_own, x_own, tol=1e-8, maxit=1000):
+        """This rank's part of the sharded PCG (collective over the ranks); f_own /
+        x_own: n_own float64 CUDA tensors on this rank's owned dofs."""
+        n = self.shard["n_own"]
+        it = C.c_int(0)
+        rel = C.c_double(0.0)
+        rc = L.lib().mdd_shard_solve(self._h, self._p(f_own, n), self._p(x_own, n), tol, maxit, 0,
+                                     C.byref(it), C.byref(rel))
+        if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
+            L.check(rc)
+        return it.value, rel.value, rc == L.MDD_OK
+
     def set_profiling(self, on=True):
         L.check(L.lib().mdd_set_profiling(self._h, 1 if on else 0))
 
@@ -245,3 +272,19 @@ class MaxwellDD:
         ln = (C.c_int64 * len(L.PROF_NAMES))()
         L.check(L.lib().mdd_profile(self._h, ms, ln, len(L.PROF_NAMES)))
         return {k: (ms[i], ln[i]) for i, k in enumerate(L.PROF_NAMES)}
+
+
+def shard_solve_group(handles, f_own, x_own, tol=1e-8, maxit=1000):
+    """Sharded PCG of several handles of this process on one GPU (handle k = rank
+    k), exchanging through device copies (mdd_shard_solve_group)."""
+    k = len(handles)
+    P = C.c_void_p
+    hs = (P * k)(*[h._h.value for h in handles])
+    fs = (P * k)(*[h._p(f, h.shard["n_own"]) for h, f in zip(handles, f_own)])
+    xs = (P * k)(*[h._p(x, h.shard["n_own"]) for h, x in zip(handles, x_own)])
+    it = C.c_int(0)
+    rel = C.c_double(0.0)
+    rc = L.lib().mdd_shard_solve_group(hs, k, fs, xs, tol, maxit, C.byref(it), C.byref(rel))
+    if rc not in (L.MDD_OK, L.MDD_ERR_NOCONV):
+        L.check(rc)
+    return it.value, rel.value, rc == L.MDD_OK

@@ -64,6 +64,10 @@ CASES_MEASURED = {
 CASES = {**CASES_LITERAL, **CASES_MEASURED}
 
 
+def is_literal_case(name):
+    return name in CASES_LITERAL
+
+
 def _holes():
     n = 8
     mask = np.ones(n ** 3, bool)

@@ -183,12 +183,14 @@ def test_profiled_eager_solve_matches_graph_solve():
 
 def test_plan_statistics_cover_every_sweep_and_factor_path():
     """Every task kind of the sweep (packed, strip, 2-D) and the blocked front
-    factorisation run in at least one oracle-compared case above (mdd_info plan
-    statistics; the c1 recipe's coarse factor has the 2-D tiles and blocked fronts)."""
+    factorisation run in at least one oracle-compared case (mdd_info plan statistics:
+    the 2-D tiles and the blocked fronts come from the coarse factors of the 16^3
+    golden cases, n0 ~ 5k-9k, compared with the oracle in test_gpu_golden.py)."""
     seen = {k: 0 for k in ("local_sn_packed", "local_sn_strip", "coarse_sn_packed", "coarse_sn_strip",
                            "coarse_sn_2d", "coarse_blocked_fronts", "local_sn_2d", "local_blocked_fronts")}
-    for name in ALL:
-        w, P, G = pair(name)
+    from parity_lib import golden_names, golden_pair
+    handles = [pair(name)[2] for name in ALL] + [golden_pair(name)[2] for name in golden_names()]
+    for G in handles:
         for k in seen:
             seen[k] += int(G.info[k])
     for k in ("local_sn_packed", "local_sn_strip", "coarse_sn_packed", "coarse_sn_strip", "coarse_sn_2d",

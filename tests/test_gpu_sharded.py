@@ -1,0 +1,73 @@
+"""The sharded PCG (sharded.cu) on one GPU: N "ranks" as N handles of this
+process exchanging halos and allreduces through device copies
+(mdd_shard_solve_group, the same kernel sequence as the NCCL path), against the
+single-handle solve of the same operator (variant as2_coarse_start, reading
+R13) and against the oracle; plus the one-rank NCCL path (the allreduces through
+a one-rank NCCL communicator)."""
+import numpy as np
+import pytest
+
+import workloads
+from parity_lib import CASES, is_literal_case, rel
+from oracle import solver as osolver
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _group(w, nranks):
+    from paper_2311_18783_b200 import MaxwellDD
+    hs = []
+    for k in range(nranks):
+        h = MaxwellDD(w, variant="as2_coarse_start")
+        h.shard_setup(k, nranks)
+        hs.append(h)
+    return hs
+
+
+@pytest.mark.parametrize("name,nranks", [("c0", 2), ("c4-lit-x2", 2), ("c4-lit-x2", 4), ("c4-recipe-x2", 2),
+                                         ("c1-recipe-8", 2)])
+def test_group_sharded_solve_matches_single_handle_and_oracle(name, nranks):
+    from paper_2311_18783_b200 import MaxwellDD
+    from paper_2311_18783_b200.solver import shard_solve_group
+    w = CASES[name]()
+    G = MaxwellDD(w, variant="as2_coarse_start")
+    f = workloads.rhs(G.n, w.f_seed)
+    x1 = torch.empty(G.n, dtype=torch.float64, device="cuda")
+    it1, rel1, ok1 = G.solve(torch.as_tensor(f, device="cuda"), x1, tol=1e-8)
+    x1 = x1.cpu().numpy()
+    hs = _group(w, nranks)
+    own = [h.owned for h in hs]
+    assert np.array_equal(np.sort(np.concatenate(own)), np.arange(G.n))
+    fo = [torch.as_tensor(f[o], device="cuda") for o in own]
+    xo = [torch.empty(len(o), dtype=torch.float64, device="cuda") for o in own]
+    it, relres, ok = shard_solve_group(hs, fo, xo, tol=1e-8)
+    x = np.zeros(G.n)
+    for o, t in zip(own, xo):
+        x[o] = t.cpu().numpy()
+    P = osolver.Problem(w)
+    xr, itr, _ = P.solve(f, tol=1e-8, x0="coarse")
+    assert ok and relres <= 1e-8 and abs(it - it1) <= 1 and abs(it - itr) <= 1, (it, it1, itr)
+    d1, dr = rel(x, x1), rel(x, xr)
+    print(f"{name} x{nranks}: iters {it} (single {it1}, oracle {itr}); vs single {d1:.1e}, vs oracle {dr:.1e}")
+    if is_literal_case(name):
+        assert d1 <= 1e-8 and dr <= 1e-8
+    else:   # the single handle's own distance to the oracle sets the scale (kappa ~ 1e10)
+        assert d1 <= 10 * max(rel(x1, xr), 1e-12) and dr <= 10 * max(rel(x1, xr), 1e-12)
+
+
+def test_one_rank_nccl_path():
+    from paper_2311_18783_b200 import MaxwellDD
+    w = CASES["c0"]()
+    h = MaxwellDD(w, variant="as2_coarse_start")
+    h.shard_setup(0, 1)
+    h.shard_nccl_init(torch.cuda.nccl.unique_id())
+    f = workloads.rhs(h.n, w.f_seed)
+    x = torch.empty(h.n, dtype=torch.float64, device="cuda")
+    it, relres, ok = h.shard_solve(torch.as_tensor(f[h.owned], device="cuda"), x)
+    G = MaxwellDD(w, variant="as2_coarse_start")
+    x1 = torch.empty(G.n, dtype=torch.float64, device="cuda")
+    it1, _, _ = G.solve(torch.as_tensor(f, device="cuda"), x1)
+    xx = np.zeros(h.n)
+    xx[h.owned] = x.cpu().numpy()
+    assert ok and it == it1 and rel(xx, x1.cpu().numpy()) <= 1e-10
