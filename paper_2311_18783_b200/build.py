@@ -13,7 +13,7 @@ EXTRA = os.environ.get("MDD_NVCC_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["mesh.cpp", "topology.cpp", "symbolic.cpp", "shard.cpp", "kernels.cu", "sweep.cu", "factor_driver.cu",
-           "geneo.cu", "geneo_lanczos.cu", "api.cu", "sharded.cu"]
+           "geneo.cu", "geneo_lanczos.cu", "coarse_e.cu", "api.cu", "sharded.cu"]
 
 
 def _newer(target, deps):

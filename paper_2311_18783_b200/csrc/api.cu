@@ -20,6 +20,7 @@
 #include "../../include/maxwell_dd.h"
 #include "device.h"
 #include "geneo.h"
+#include "coarse_e.h"
 #include "handle.h"
 #include "shard.h"
 #include "topology.h"
@@ -44,202 +45,6 @@ double now_s() {
 const double kCoarsePivotTol = 1e-14;
 
 
-// --------------------------------------------------- cuSPARSE SpGEMM helper
-struct DevCsr {
-  int64_t rows = 0, cols = 0, nnz = 0;
-  DBuf<int> ptr, idx;
-  DBuf<double> val;
-};
-
-// non-owning view of a device CSR (row-chunk slices of a DevCsr)
-struct CsrView {
-  int64_t rows = 0, cols = 0, nnz = 0;
-  int* ptr = nullptr;
-  int* idx = nullptr;
-  double* val = nullptr;
-};
-CsrView view(const DevCsr& A) { return CsrView{A.rows, A.cols, A.nnz, A.ptr.p, A.idx.p, A.val.p}; }
-
-// C = A B with cuSPARSE SpGEMM.  ALG1 (the default) needs workspace that grows
-// with the intermediate products and reports INSUFFICIENT_RESOURCES on the large
-// coarse products; then ALG2 and finally the chunked ALG3 are used.
-void spgemm(cusparseHandle_t H, const CsrView& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
-            const char* what) {
-  CUSPARSE_CHECK(cusparseSetStream(H, s));
-  const cusparseSpGEMMAlg_t algs[3] = {CUSPARSE_SPGEMM_DEFAULT, CUSPARSE_SPGEMM_ALG2,
-                                       CUSPARSE_SPGEMM_ALG3};
-  std::string errs;
-  for (int ai = 0; ai < 3; ++ai) {
-    const cusparseSpGEMMAlg_t alg = algs[ai];
-    cusparseSpMatDescr_t a, b, c;
-    CUSPARSE_CHECK(cusparseCreateCsr(&a, A.rows, A.cols, A.nnz, A.ptr, A.idx, A.val,
-                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-    CUSPARSE_CHECK(cusparseCreateCsr(&b, B.rows, B.cols, B.nnz, B.ptr.p, B.idx.p, B.val.p,
-                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-    C.rows = A.rows; C.cols = B.cols;
-    C.ptr.alloc(C.rows + 1);
-    CUSPARSE_CHECK(cusparseCreateCsr(&c, C.rows, C.cols, 0, C.ptr.p, nullptr, nullptr,
-                                     CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO, CUDA_R_64F));
-    cusparseSpGEMMDescr_t d;
-    CUSPARSE_CHECK(cusparseSpGEMM_createDescr(&d));
-    double one = 1.0, zero = 0.0;
-    auto op = CUSPARSE_OPERATION_NON_TRANSPOSE;
-    size_t b1 = 0, b2 = 0, b3 = 0;
-    DBuf<char> w1, w2, w3;
-    cusparseStatus_t st = cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F,
-                                                        alg, d, &b1, nullptr);
-    if (st == CUSPARSE_STATUS_SUCCESS) {
-      w1.alloc(std::max<size_t>(b1, 1));
-      st = cusparseSpGEMM_workEstimation(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b1, w1.p);
-    }
-    if (st == CUSPARSE_STATUS_SUCCESS && alg != CUSPARSE_SPGEMM_DEFAULT) {
-      // ALG2 / ALG3: the compute buffer size comes from estimateMemory; buffer 1
-      // stays alive until the copy
-      int64_t nprod = 0;
-      st = cusparseSpGEMM_getNumProducts(d, &nprod);
-      if (st == CUSPARSE_STATUS_SUCCESS)
-        st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
-                                           &b3, nullptr, nullptr);
-      if (st == CUSPARSE_STATUS_SUCCESS) {
-        w3.alloc(std::max<size_t>(b3, 1));
-        st = cusparseSpGEMM_estimateMemory(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, 0.2f,
-                                           &b3, w3.p, &b2);
-        w3.release();
-      }
-    } else if (st == CUSPARSE_STATUS_SUCCESS) {
-      st = cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b2, nullptr);
-    }
-    if (st == CUSPARSE_STATUS_SUCCESS) {
-      w2.alloc(std::max<size_t>(b2, 1));
-      st = cusparseSpGEMM_compute(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d, &b2, w2.p);
-    }
-    int64_t r_ = 0, c_ = 0, nnz = 0;
-    if (st == CUSPARSE_STATUS_SUCCESS) st = cusparseSpMatGetSize(c, &r_, &c_, &nnz);
-    if (st == CUSPARSE_STATUS_SUCCESS) {
-      C.nnz = nnz;
-      C.idx.alloc(std::max<int64_t>(nnz, 1));
-      C.val.alloc(std::max<int64_t>(nnz, 1));
-      st = cusparseCsrSetPointers(c, C.ptr.p, C.idx.p, C.val.p);
-    }
-    if (st == CUSPARSE_STATUS_SUCCESS)
-      st = cusparseSpGEMM_copy(H, op, op, &one, a, b, &zero, c, CUDA_R_64F, alg, d);
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    cusparseSpGEMM_destroyDescr(d);
-    cusparseDestroySpMat(a); cusparseDestroySpMat(b); cusparseDestroySpMat(c);
-    if (st == CUSPARSE_STATUS_SUCCESS) return;
-    errs += " alg" + std::to_string(ai) + ":status " + std::to_string((int)st);
-    if (st != CUSPARSE_STATUS_INSUFFICIENT_RESOURCES && st != CUSPARSE_STATUS_NOT_SUPPORTED) break;
-  }
-  throw Error(1, std::string("cuSPARSE SpGEMM failed for ") + what + " (" + std::to_string(A.rows) +
-                     "x" + std::to_string(A.cols) + " nnz " + std::to_string(A.nnz) + " times " +
-                     std::to_string(B.rows) + "x" + std::to_string(B.cols) + " nnz " +
-                     std::to_string(B.nnz) + "):" + errs);
-}
-
-// C = A B by row chunks of A.  A chunk holds at most max_prod intermediate
-// products (sum over its entries a_ik of nnz(B row k)), which bounds cuSPARSE's
-// workspace (the single product of the c2 coarse matrix ran out of it); the
-// chunks' CSR pieces are concatenated in row order (same entries, same values
-// as the unchunked product: each output row is computed by one call).
-void spgemm_rows(cusparseHandle_t H, const DevCsr& A, const DevCsr& B, DevCsr& C, cudaStream_t s,
-                 const char* what) {
-  // MDD_SPGEMM_MAX_PROD: test knob (forces chunking on small problems)
-  const int64_t max_prod = env_int("MDD_SPGEMM_MAX_PROD", 48 << 20);
-  std::vector<int> ap(A.rows + 1), bp(B.rows + 1), ai(A.nnz);
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  CUDA_CHECK(cudaMemcpy(ap.data(), A.ptr.p, ap.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  CUDA_CHECK(cudaMemcpy(bp.data(), B.ptr.p, bp.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  if (A.nnz) CUDA_CHECK(cudaMemcpy(ai.data(), A.idx.p, ai.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  std::vector<int64_t> cut{0};
-  int64_t acc = 0;
-  for (int64_t r = 0; r < A.rows; ++r) {
-    int64_t pr = 0;
-    for (int k = ap[r]; k < ap[r + 1]; ++k) pr += bp[ai[k] + 1] - bp[ai[k]];
-    if (acc + pr > max_prod && r > cut.back()) { cut.push_back(r); acc = 0; }
-    acc += pr;
-  }
-  cut.push_back(A.rows);
-  if (cut.size() == 2) {
-    spgemm(H, view(A), B, C, s, what);
-    return;
-  }
-  std::vector<DevCsr> parts(cut.size() - 1);
-  std::vector<int64_t> pnnz(parts.size());
-  int64_t tot = 0;
-  for (size_t c = 0; c + 1 < cut.size(); ++c) {
-    const int64_t r0 = cut[c], r1 = cut[c + 1];
-    std::vector<int> rp(r1 - r0 + 1);
-    for (int64_t r = r0; r <= r1; ++r) rp[r - r0] = ap[r] - ap[r0];
-    DBuf<int> dptr;
-    dptr.upload(rp);
-    CsrView Ac{r1 - r0, A.cols, (int64_t)(ap[r1] - ap[r0]), dptr.p, A.idx.p + ap[r0], A.val.p + ap[r0]};
-    spgemm(H, Ac, B, parts[c], s, what);
-    pnnz[c] = parts[c].nnz;
-    tot += parts[c].nnz;
-  }
-  MDD_REQUIRE(tot < INT32_MAX, 5, std::string(what) + ": product too large for 32-bit CSR offsets");
-  C.rows = A.rows; C.cols = B.cols; C.nnz = tot;
-  std::vector<int> cp(A.rows + 1, 0);
-  int64_t off = 0;
-  for (size_t c = 0; c < parts.size(); ++c) {
-    std::vector<int> pp(parts[c].rows + 1);
-    CUDA_CHECK(cudaMemcpy(pp.data(), parts[c].ptr.p, pp.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    for (int64_t r = 0; r < parts[c].rows; ++r) cp[cut[c] + r + 1] = (int)(off + pp[r + 1]);
-    off += pnnz[c];
-  }
-  C.ptr.upload(cp);
-  C.idx.alloc(std::max<int64_t>(tot, 1));
-  C.val.alloc(std::max<int64_t>(tot, 1));
-  off = 0;
-  for (size_t c = 0; c < parts.size(); ++c) {
-    if (pnnz[c]) {
-      CUDA_CHECK(cudaMemcpyAsync(C.idx.p + off, parts[c].idx.p, pnnz[c] * sizeof(int), cudaMemcpyDeviceToDevice, s));
-      CUDA_CHECK(cudaMemcpyAsync(C.val.p + off, parts[c].val.p, pnnz[c] * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    }
-    off += pnnz[c];
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    parts[c] = DevCsr();
-  }
-}
-
-void transpose(cusparseHandle_t H, const DevCsr& A, DevCsr& T, cudaStream_t s) {
-  CUSPARSE_CHECK(cusparseSetStream(H, s));
-  T.rows = A.cols; T.cols = A.rows; T.nnz = A.nnz;
-  T.ptr.alloc(T.rows + 1);
-  T.idx.alloc(std::max<int64_t>(A.nnz, 1));
-  T.val.alloc(std::max<int64_t>(A.nnz, 1));
-  size_t bs = 0;
-  CUSPARSE_CHECK(cusparseCsr2cscEx2_bufferSize(H, A.rows, A.cols, A.nnz, A.val.p, A.ptr.p, A.idx.p,
-                                               T.val.p, T.ptr.p, T.idx.p, CUDA_R_64F,
-                                               CUSPARSE_ACTION_NUMERIC, CUSPARSE_INDEX_BASE_ZERO,
-                                               CUSPARSE_CSR2CSC_ALG1, &bs));
-  DBuf<char> w; w.alloc(std::max<size_t>(bs, 1));
-  CUSPARSE_CHECK(cusparseCsr2cscEx2(H, A.rows, A.cols, A.nnz, A.val.p, A.ptr.p, A.idx.p, T.val.p,
-                                    T.ptr.p, T.idx.p, CUDA_R_64F, CUSPARSE_ACTION_NUMERIC,
-                                    CUSPARSE_INDEX_BASE_ZERO, CUSPARSE_CSR2CSC_ALG1, w.p));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-}
-
-// CSR (int32 pointers) download + sort each row; returns pattern and value slot
-void download_sorted(const DevCsr& C, Csr& pat, std::vector<int64_t>& slot) {
-  std::vector<int> ptr(C.rows + 1), idx(C.nnz);
-  CUDA_CHECK(cudaMemcpy(ptr.data(), C.ptr.p, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  if (C.nnz) CUDA_CHECK(cudaMemcpy(idx.data(), C.idx.p, idx.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  pat.nrows = (int)C.rows; pat.ncols = (int)C.cols;
-  pat.ptr.assign(C.rows + 1, 0);
-  pat.idx.resize(C.nnz);
-  slot.resize(C.nnz);
-  for (int64_t r = 0; r < C.rows; ++r) {
-    std::vector<std::pair<int, int64_t>> row;
-    for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) row.push_back({idx[k], k});
-    std::sort(row.begin(), row.end());
-    for (size_t j = 0; j < row.size(); ++j) {
-      pat.idx[ptr[r] + j] = row[j].first;
-      slot[ptr[r] + j] = row[j].second;
-    }
-    pat.ptr[r + 1] = ptr[r + 1];
-  }
-}
 
 }  // namespace
 
@@ -529,7 +334,7 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
     const int64_t nb = H->grad_rank + H->ngeneo;
     H->n0 = nb;
     MDD_REQUIRE(nb > 0, 2, "empty coarse space");
-    DevCsr Z, Zt, W, E;
+    DevCsr Z, Zt, W, E, Zgd;
     {
       // assemble Z in CSR by dof: gradient entries sign/mult (computed in double on
       // the host as the exact quotient of two small integers), GenEO entries from
@@ -571,6 +376,19 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       for (int e = 0; e <= n; ++e) rptr[e] = (int)rp[e];
       Z.rows = n; Z.cols = nb; Z.nnz = nnz;
       Z.ptr.upload(rptr); Z.idx.upload(ridx); Z.val.upload(rval);
+      {
+        // the gradient columns alone (block assembly of E)
+        std::vector<int> gp(n + 1, 0), gi;
+        std::vector<double> gv;
+        for (int e = 0; e < n; ++e) {
+          for (int64_t q = rp[e]; q < rp[e + 1]; ++q)
+            if (ridx[q] < H->grad_rank) { gi.push_back(ridx[q]); gv.push_back(rval[q]); }
+          gp[e + 1] = (int)gi.size();
+        }
+        Zgd.rows = n; Zgd.cols = H->grad_rank; Zgd.nnz = (int64_t)gi.size();
+        Zgd.ptr.upload(gp); Zgd.idx.upload(gi.empty() ? std::vector<int>{0} : gi);
+        Zgd.val.upload(gv.empty() ? std::vector<double>{0.0} : gv);
+      }
       if (H->ngeneo > 0) {
         // GenEO values: Z.val[dst[k]] = blocks[src[k]] on the device
         DBuf<double> blocks;
@@ -589,7 +407,6 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
         dev::k_scatter_gather<<<nblk((int64_t)gsrc.size(), 256), 256, 0, s>>>((int64_t)gsrc.size(), ddst.p, dsrc.p, blocks.p, Z.val.p);
         CUDA_CHECK(cudaStreamSynchronize(s));
       }
-      for (int i = 0; i < nsub; ++i) geneo[i].W.release();
     }
     // E = Z^T (A Z) via cuSPARSE SpGEMM
     {
@@ -601,10 +418,39 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       Ad.idx.upload(H->Apat.idx);
       Ad.val.alloc(Ad.nnz);
       CUDA_CHECK(cudaMemcpyAsync(Ad.val.p, H->A_val.p, Ad.nnz * sizeof(double), cudaMemcpyDeviceToDevice, s));
-      spgemm_rows(H->sp, Ad, Z, W, s, "A Z");
       transpose(H->sp, Z, Zt, s);
-      spgemm_rows(H->sp, Zt, W, E, s, "Z^T (A Z)");
-      W = DevCsr();
+      const char* ea = getenv("MDD_E_ASSEMBLY");
+      if (ea && std::string(ea) == "spgemm") {
+        // one sparse product through the dense GenEO columns (reference path)
+        spgemm_rows(H->sp, Ad, Z, W, s, "A Z");
+        spgemm_rows(H->sp, Zt, W, E, s, "Z^T (A Z)");
+        W = DevCsr();
+      } else {
+        // by blocks: E_gg sparse, E_gi and E_ij through dense products (coarse_e.cu);
+        // subdomains i, j can couple when Omega_i and Omega_j grown by one cube layer meet
+        DevCsr Zgt;
+        transpose(H->sp, Zgd, Zgt, s);
+        std::vector<int32_t> nptr(1, 0), nbr;
+        const int sx = m.nx / d->px, sy = m.ny / d->py, sz = m.nz / d->pz, o = d->overlap;
+        for (int i = 0; i < nsub; ++i) {
+          const int ii[3] = {i % d->px, (i / d->px) % d->py, i / (d->px * d->py)};
+          for (int j = 0; j < nsub; ++j) {
+            const int jj[3] = {j % d->px, (j / d->px) % d->py, j / (d->px * d->py)};
+            const int sz3[3] = {sx, sy, sz};
+            bool meet = true;
+            for (int a = 0; a < 3; ++a) {
+              const int lo_i = ii[a] * sz3[a] - o, hi_i = (ii[a] + 1) * sz3[a] + o;
+              const int lo_j = jj[a] * sz3[a] - o - 1, hi_j = (jj[a] + 1) * sz3[a] + o + 1;
+              meet &= lo_i < hi_j && lo_j < hi_i;
+            }
+            if (meet) nbr.push_back(j);
+          }
+          nptr.push_back((int32_t)nbr.size());
+        }
+        coarse_E_blocks(H->sp, Ad, H->Apat, Zgd, Zgt, H->dec.sub_dofs, geneo, nptr, nbr, s, E);
+      }
+      Zgd = DevCsr();
+      for (int i = 0; i < nsub; ++i) geneo[i].W.release();
       // Jacobi scaling E <- S E S, Z <- Z S (S = diag(E)^{-1/2}): the coarse operator
       // Z E^{-1} Z^T is unchanged, the factorised matrix has a unit diagonal
       DBuf<double> sc;

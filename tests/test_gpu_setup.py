@@ -52,3 +52,28 @@ def test_block_lanczos_geneo_matches_the_oracle(name):
     else:
         assert m["lz_lambda_rel"] <= max(10 * OBSERVED[name]["geneo_lambda_rel"], 1e-8), m
         assert m["lz_prec_vs_oracle"] <= 10 * OBSERVED[name]["prec_as2_fwd_gpu"] + 10 * OBSERVED[name]["local_fwd_gpu"], m
+
+
+@pytest.mark.parametrize("name", ["c1-recipe-8", "c4-recipe-x2", "c3-recipe-12"])
+def test_block_assembly_of_E_matches_the_sparse_product(name):
+    """E = Z^T A Z assembled by blocks (E_gg sparse, E_gi / E_ij through dense
+    products per subdomain pair, coarse_e.cu; the default) equals the single
+    sparse product Z^T (A Z) (MDD_E_ASSEMBLY=spgemm) up to summation order, and
+    the two handles solve alike."""
+    from paper_2311_18783_b200 import MaxwellDD
+    from parity_lib import CASES
+    w = CASES[name]()
+    G0 = MaxwellDD(w)
+    os.environ["MDD_E_ASSEMBLY"] = "spgemm"
+    try:
+        G1 = MaxwellDD(w)
+    finally:
+        os.environ.pop("MDD_E_ASSEMBLY", None)
+    assert G0.info["ngeneo"] > 0 and G0.info["n0"] == G1.info["n0"]
+    E0, E1 = G0.coarse_matrix(), G1.coarse_matrix()
+    assert abs(E0 - E1).max() <= 1e-12 * abs(E1).max()
+    assert abs(E0 - E0.T).max() <= 1e-12 * abs(E0).max()
+    f = workloads.rhs(G0.n, w.f_seed)
+    x0, it0, _ = G0.solve_host(f)
+    x1, it1, _ = G1.solve_host(f)
+    assert abs(it0 - it1) <= 1 and np.linalg.norm(x0 - x1) <= 1e-6 * np.linalg.norm(x1)
