@@ -307,6 +307,12 @@ def main():
 
     info = G.info
     roof = roofline(G, sweep_ms, in_step)
+    # the whole PCG iteration against the same roofline: algorithmic bytes of one
+    # iteration (MaxwellDD.bytes_model) x iterations / device time
+    bm = G.bytes_model()
+    it_gbs = bm["iteration"] * iters[-1] / (step_ms / 1e3) / 1e9
+    roof["iteration"] = {"bytes_per_iteration": bm["iteration"], "achieved": it_gbs,
+                         "frac": it_gbs / roof["peak"], "breakdown_bytes": bm}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
@@ -327,7 +333,11 @@ def main():
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches,
+        "kernels_per_iteration": int(info.get("kernels_per_iter", 0)),
         "clocks": clocks,
+        "paper_context": ("PAPER.md §4 (FreeFEM/PETSc GMRES on CPUs, hexahedral beam meshes): "
+                          "AS-SNK-GenEO takes 23-28 iterations across Tables 3-7; ~300 GenEO "
+                          "vectors per subdomain in the mu_alt = 1e4 case (Table 5); context only"),
     }
     if rank == 0 and not args.no_cpu_baseline:
         v, desc, cores, _ = cpu_oracle_sample(args.config, variant=args.variant)
@@ -353,6 +363,7 @@ def roofline(G, sweep_ms, in_step):
         pass
     b = G.bytes_model()["local"]
     achieved = b / (sweep_ms / 1e3) / 1e9
+    achieved_in_step = b / (in_step[0] / 1e3) / 1e9 if in_step[0] > 0 else None
     traffic = None
     try:  # DRAM bytes of one k_sweep (local) launch from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_sweep_local.json")) as fh:
@@ -363,6 +374,8 @@ def roofline(G, sweep_ms, in_step):
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": src, "bytes_per_launch": b,
             "avg_launch_ms": sweep_ms, "avg_launch_ms_in_step": in_step[0],
+            "achieved_in_step": achieved_in_step,
+            "frac_in_step": achieved_in_step / peak if achieved_in_step else None,
             "launches_in_step": in_step[1]}
 
 

@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <map>
 #include <numeric>
 
 namespace mdd {
@@ -393,8 +394,62 @@ void build_factor_plan(FactorPlan& fp, const std::vector<SymSystem>& systems, in
   }
   fp.lsize = fp.sn_lptr[fp.nsn];
   fp.usize = fp.sn_uptr[fp.nsn];
-  fp.fsize = fp.sn_fptr[fp.nsn];
-  fp.umsize = fp.sn_umptr[fp.nsn];
+  // The numeric factorisation runs level by level, so a front is live during its
+  // level only (level-local offsets; peak = the largest level), and an update
+  // matrix from its supernode's level until its parent's level has assembled it
+  // (first-fit offsets over those lifetimes; peak = the most live at one level).
+  // Summing every front and update matrix instead ran out of the 180 GB on the
+  // c4 coarse factor.
+  {
+    i64 fmax = 0;
+    for (int l = 0; l < fp.nlevels; ++l) {
+      i64 off = 0;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        const i64 nr = (i64)fp.sn_ncol[g] + fp.sn_noff[g];
+        fp.sn_fptr[g] = off;
+        off += nr * nr;
+      }
+      fmax = std::max(fmax, off);
+    }
+    fp.sn_fptr[fp.nsn] = fmax;
+    fp.fsize = fmax;
+    std::map<i64, i64> freel;  // offset -> length of the free blocks
+    i64 top = 0;
+    std::vector<std::vector<int>> release(fp.nlevels + 2);
+    auto give_back = [&](i64 off, i64 len) {
+      auto it = freel.emplace(off, len).first;
+      auto nx = std::next(it);
+      if (nx != freel.end() && it->first + it->second == nx->first) { it->second += nx->second; freel.erase(nx); }
+      if (it != freel.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) { pv->second += it->second; freel.erase(it); }
+      }
+    };
+    for (int l = 0; l < fp.nlevels; ++l) {
+      for (int g : release[l]) give_back(fp.sn_umptr[g], (i64)fp.sn_noff[g] * fp.sn_noff[g]);
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        const i64 len = (i64)fp.sn_noff[g] * fp.sn_noff[g];
+        if (len == 0) { fp.sn_umptr[g] = 0; continue; }
+        auto it = freel.begin();
+        while (it != freel.end() && it->second < len) ++it;
+        if (it != freel.end()) {
+          const i64 off = it->first, rest = it->second - len;
+          freel.erase(it);
+          if (rest > 0) freel.emplace(off + len, rest);
+          fp.sn_umptr[g] = off;
+        } else {
+          fp.sn_umptr[g] = top;
+          top += len;
+        }
+        const int lp = fp.sn_parent[g] == -1 ? l : fp.sn_level[fp.sn_parent[g]];
+        release[lp + 1].push_back(g);
+      }
+    }
+    fp.sn_umptr[fp.nsn] = top;
+    fp.umsize = top;
+  }
   // relative maps: position of each off row of g in its parent's row list
   fp.relmap_ptr = fp.sn_rowptr;
   fp.relmap.assign(fp.offrows.size(), -1);

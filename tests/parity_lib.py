@@ -334,7 +334,8 @@ def golden_workloads():
 
 def golden_names():
     import os
-    return sorted(f[:-5] for f in os.listdir(GOLDEN_DIR) if f.endswith(".json")) if os.path.isdir(GOLDEN_DIR) else []
+    return sorted(f[:-5] for f in os.listdir(GOLDEN_DIR)
+                  if f.endswith(".json") and not f.startswith("geneo_")) if os.path.isdir(GOLDEN_DIR) else []
 
 
 _gcache = {}
