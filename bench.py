@@ -9,10 +9,13 @@ separately under "setup_s".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl b200|reference]
 
-N = 1: BASELINE.json configs[1] (c1: 32^3 cubes x 6 tets, 4^3 subdomains).
+N = 1: BASELINE.json configs[4] at one GPU (c4: 64^3 cubes x 6 tets, 4^3
+subdomains, 1.8M dofs, 20k GenEO vectors) -- the largest single-GPU config
+(c3, 96^3 / 512 subdomains, is the 8-GPU mesh); --config c1 / c2 for the others.
 N > 1 (torchrun, one rank per GPU): every rank solves its own replica of the
-workload (no data-path collective; the sharded solve is not built yet), value =
-all ranks' DOF*iterations / max-over-ranks time, "scaling": "weak".
+workload (weak scaling, no data-path collective: the sharded solve of sharded.cu
+replicates the setup and the coarse factor, so c4_weak64_xN does not fit it --
+DESIGN.md §9), value = all ranks' DOF*iterations / max-over-ranks time.
 
 --impl reference times the CPU oracle (oracle/, fp64 numpy/scipy) on a bounded
 sample of the same recipe on rank 0; other ranks exit 0.
@@ -40,7 +43,10 @@ UNIT = "DOF*iter/s"
 TOL = 1e-8
 # the oracle sample: the c1 recipe (channels, contrast 1e4, gamma 1e-4, overlap 1,
 # threshold 0.1) on a 12^3 grid with 2^3 subdomains (setup untimed)
-CPU_SAMPLE = dict(n=12, p=2)
+# the oracle sample per recipe: the same coefficients / gamma / overlap / threshold on a
+# grid the oracle's dense GEVPs finish in seconds (setup untimed)
+CPU_SAMPLES = {"c1": dict(n=12, p=2), "c2": dict(n=12, p=2, hole=2), "c3": dict(n=12, p=2),
+               "c4": dict(m=12, q=2)}
 
 
 def _env_int(k, d):
@@ -55,7 +61,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c1")
+    # c4 at N = 1 (64^3 cubes, 4^3 subdomains, 1.8M dofs): the largest single-GPU
+    # configuration of BASELINE.json (c3 is the 8-GPU mesh)
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # as2_coarse_start: M_AS,2 (eq. 2.4) with PCG started from x0 = Q f, one coarse
@@ -113,7 +121,7 @@ def cpu_oracle_sample(cfg, max_seconds=30.0, min_solves=1, variant="as2_coarse_s
     sample; returns (DOF*iter/s, description, cores)."""
     import threadpoolctl  # noqa: F401  (scipy/numpy BLAS pools are used as they stand)
     from oracle import solver as osolver
-    w = workloads.make(cfg, **CPU_SAMPLE) if cfg in ("c1",) else workloads.make(cfg)
+    w = workloads.make(cfg, **CPU_SAMPLES.get(cfg, {}))
     t0 = time.perf_counter()
     P = osolver.Problem(w, variant="as2" if variant == "as2_coarse_start" else variant)
     x0 = "coarse" if variant == "as2_coarse_start" else "zero"
@@ -151,7 +159,7 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg + "_oracle_sample", "recipe": cfg, **CPU_SAMPLE},
+            "config": {"workload": cfg + "_oracle_sample", "recipe": cfg, **CPU_SAMPLES.get(cfg, {})},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -223,6 +231,7 @@ def main():
     clk = Clocks(local)
     clk.start()
     sw0 = G.sweep_timing("local")
+    cw0 = G.sweep_timing("coarse") if G.info["n0"] else (0.0, 0)
     t_ms = 0.0
     launches = 0
     work = 0
@@ -241,6 +250,7 @@ def main():
         iters.append(it)
     torch.cuda.synchronize()
     sw1 = G.sweep_timing("local")
+    cw1 = G.sweep_timing("coarse") if G.info["n0"] else (0.0, 0)
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
@@ -248,22 +258,30 @@ def main():
     step_ms_max, total_work = reduce_over_ranks(step_ms, work, world, "cuda")
     value = total_work / (step_ms_max * args.steps / 1e3)
     in_step = ((sw1[0] - sw0[0]) / max(1, sw1[1] - sw0[1]), sw1[1] - sw0[1])
+    cin_step = ((cw1[0] - cw0[0]) / max(1, cw1[1] - cw0[1]), cw1[1] - cw0[1])
 
-    # ---- the dominant kernel alone: the persistent sweep of the local solves
-    # (one k_sweep launch per mdd_apply_local), CUDA events on its stream
+    # ---- the two persistent sweeps alone (one k_sweep launch each): the local
+    # solves (mdd_apply_local) and the coarse solve E^{-1} (mdd_apply_coarse_inverse),
+    # CUDA events on their stream
+    def timed(fn, reps=10):
+        for _ in range(2):
+            fn()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
     v = torch.randn(n, dtype=torch.float64, device="cuda")
     y = torch.empty_like(v)
-    for _ in range(3):
-        G.apply_local(v, y)
-    reps = 20
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        G.apply_local(v, y)
-    e1.record(stream)
-    e1.synchronize()
-    sweep_ms = e0.elapsed_time(e1) / reps
+    sweep_ms = timed(lambda: G.apply_local(v, y))
+    n0 = int(G.info["n0"])
+    v0 = torch.randn(max(n0, 1), dtype=torch.float64, device="cuda")
+    y0 = torch.empty_like(v0)
+    csweep_ms = timed(lambda: G.apply_coarse_inverse(v0, y0)) if n0 else None
+    csw1 = G.sweep_timing("coarse") if n0 else None
     # per-phase breakdown of one solve (eager path with events; not the timed path)
     G.set_profiling(True)
     G.solve(f, x, tol=TOL, maxit=args.maxit)
@@ -306,7 +324,7 @@ def main():
         G.set_variant(args.variant)
 
     info = G.info
-    roof = roofline(G, sweep_ms, in_step)
+    roof = roofline(G, sweep_ms, in_step, csweep_ms, cin_step, t_ms)
     # the whole PCG iteration against the same roofline: algorithmic bytes of one
     # iteration (MaxwellDD.bytes_model) x iterations / device time
     bm = G.bytes_model()
@@ -350,10 +368,11 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(G, sweep_ms, in_step):
-    """Dominant kernel of the step -- the persistent supernodal sweep applying
-    M_AS (k_sweep, one launch per preconditioner application) -- against the
-    measured HBM copy bandwidth (MEASURED_PEAKS.json)."""
+def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=None):
+    """Dominant kernel of the step against the measured HBM copy bandwidth
+    (MEASURED_PEAKS.json): of the two persistent supernodal sweeps (k_sweep) -- the
+    local solves M_AS and the coarse solve E^{-1}, one launch each per PCG
+    iteration -- the one with the larger share of the step's device time."""
     peak, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -361,8 +380,18 @@ def roofline(G, sweep_ms, in_step):
             src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         pass
+    info = G.info
     b = G.bytes_model()["local"]
     achieved = b / (sweep_ms / 1e3) / 1e9
+    # the coarse sweep: every factor entry of E once per direction + the right-hand
+    # side and solution in coarse positions
+    cb = 2 * 8 * info["coarse_factor_nnz"] + 16 * info["n0"]
+    coarse = None
+    if csweep_ms:
+        c_in = cb / (cin_step[0] / 1e3) / 1e9 if cin_step[0] > 0 else None
+        coarse = {"kernel": "k_sweep (coarse solve E^-1)", "bytes_per_launch": cb, "avg_launch_ms": csweep_ms,
+                  "achieved": cb / (csweep_ms / 1e3) / 1e9, "avg_launch_ms_in_step": cin_step[0],
+                  "achieved_in_step": c_in, "launches_in_step": cin_step[1]}
     achieved_in_step = b / (in_step[0] / 1e3) / 1e9 if in_step[0] > 0 else None
     traffic = None
     try:  # DRAM bytes of one k_sweep (local) launch from the committed ncu capture
@@ -370,13 +399,29 @@ def roofline(G, sweep_ms, in_step):
             traffic = float(json.load(fh)["dram_bytes_per_launch"])
     except Exception:
         pass
-    return {"bound": "hbm", "kernel": "k_sweep (local solves: gather, L y = b, D^-1, L^T x = z, prolong)",
-            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": src, "bytes_per_launch": b,
-            "avg_launch_ms": sweep_ms, "avg_launch_ms_in_step": in_step[0],
-            "achieved_in_step": achieved_in_step,
-            "frac_in_step": achieved_in_step / peak if achieved_in_step else None,
-            "launches_in_step": in_step[1]}
+    local = {"kernel": "k_sweep (local solves: gather, L y = b, D^-1, L^T x = z, prolong)",
+             "achieved": achieved, "bytes_per_launch": b,
+             "avg_launch_ms": sweep_ms, "avg_launch_ms_in_step": in_step[0],
+             "achieved_in_step": achieved_in_step, "launches_in_step": in_step[1]}
+    # dominant = the larger in-step total time (launches x in-kernel duration)
+    tl = in_step[0] * in_step[1]
+    tc = cin_step[0] * cin_step[1] if coarse else 0.0
+    main, other = (coarse, local) if coarse and tc > tl else (local, coarse)
+    for k in (main, other):
+        if k:
+            k["frac"] = k["achieved"] / peak
+            k["frac_in_step"] = k["achieved_in_step"] / peak if k["achieved_in_step"] else None
+            if total_ms:   # in-kernel time of all its launches / the timed region's device time
+                k["share_of_step"] = k["avg_launch_ms_in_step"] * k["launches_in_step"] / total_ms
+    if traffic is not None and main is not local:
+        traffic = None  # the committed ncu capture is of the local sweep
+    out = {"bound": "hbm", "kernel": main["kernel"], "achieved": main["achieved"], "peak": peak, "unit": "GB/s",
+           "frac": main["achieved"] / peak, "traffic": traffic, "peak_source": src,
+           "bytes_per_launch": main["bytes_per_launch"], "avg_launch_ms": main["avg_launch_ms"],
+           "avg_launch_ms_in_step": main["avg_launch_ms_in_step"], "achieved_in_step": main["achieved_in_step"],
+           "frac_in_step": main["frac_in_step"], "launches_in_step": main["launches_in_step"],
+           "other_sweep": other}
+    return out
 
 
 if __name__ == "__main__":

