@@ -94,7 +94,8 @@ int mdd_setup(const mdd_setup_desc* desc, mdd_handle* out);
 
 void mdd_destroy(mdd_handle h);
 
-/* Preconditioned CG (x0 = 0) on A x = f with the configured preconditioner,
+/* Preconditioned CG on A x = f with the configured preconditioner (x0 = 0, or
+ * x0 = Q f for MDD_VARIANT_AS2_COARSE_START),
  * stopping at ||r_k||_2 <= tol ||f||_2 or maxit.  f, x: DEVICE pointers to n
  * doubles (n = free dofs, MDD_INFO_N).  *iters, *relres: HOST outputs.  Runs on
  * the handle's stream and synchronises it before returning. */

@@ -17,7 +17,9 @@ largest node (span unchanged, G_i full rank); R8 the SNK family is linearly
 dependent (e.g. identical columns of a node deep in an overlap), so the coarse
 operator is Z E^+ Z^T with E^+ a generalised inverse -- the operator is the same
 for every basis / g-inverse (Z E^- Z^T A is the A-orthogonal projection on V_0).
-The oracle computes E^+ by a dense Hermitian pseudo-inverse of the Jacobi-scaled E.
+The oracle takes a basis of V_0 (eigenvectors of the exact integer Gram of the
+gradient candidates, gradient_rank_basis) so that E is SPD, and solves with its
+dense Cholesky factor (scipy.linalg.cho_factor).
 """
 from __future__ import annotations
 

@@ -8,7 +8,7 @@ PAPER.md
 * Initial guess (reading R13, the paper does not fix one): x0 = 0, or the
   coarse-space Galerkin solution x0 = Q f ("coarse").  From x0 = Q f one has
   Z^T r_k = 0 for every k, so M_AS,2 r_k = (I - Q A) M_AS r_k (the balancing
-  identity of Mandel's BDD; tests/test_oracle_solver.py pins it); the oracle
+  identity of Mandel's BDD; tests/test_oracle_dd_coarse_pcg.py pins it); the oracle
   still applies the full eq. (2.4) operator in either case.
 The "additive" variant sum_i R_i^T A_i^{-1} R_i + Z E^{-1} Z^T is north_star's
 written form without D_i (reading R1); it is exposed for comparison only.

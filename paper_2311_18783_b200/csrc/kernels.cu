@@ -392,15 +392,6 @@ __global__ void k_front_fold_d(PlanDev P, int g, double* __restrict__ L, const d
   }
 }
 
-__global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
-                          const double* __restrict__ x, double* __restrict__ out) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  double s = 0.0;
-  for (int64_t k = ptr[e]; k < ptr[e + 1]; ++k) s += x[pos[k]];
-  out[e] = s;
-}
-
 // ---------------------------------------------------------- PCG pieces
 #define STOPPED (stop != nullptr && stop[0] != 0)
 
@@ -445,27 +436,6 @@ __device__ void reduce_step_tail(const double* part, const RedStep& rs) {
     scalar_op(rs.op, rs.S, rs.state);
     *rs.counter = 0u;
   }
-}
-
-// y = A x, one warp per row; optional partial dot(dotw, y)
-__global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                       const double* __restrict__ val, const double* __restrict__ x,
-                       double* __restrict__ y, const double* __restrict__ dotw,
-                       double* __restrict__ part, const int* __restrict__ stop) {
-  if (STOPPED) return;
-  const int lane = threadIdx.x & 31;
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  double contrib = 0.0;
-  if (row < n) {
-    double s = 0.0;
-    for (int64_t k = ptr[row] + lane; k < ptr[row + 1]; k += 32) s += val[k] * x[idx[k]];
-    s = warp_sum(s);
-    if (lane == 0) {
-      y[row] = s;
-      if (dotw) contrib = dotw[row] * s;
-    }
-  }
-  if (part) block_sum_store(contrib, part);
 }
 
 // y = M x with TPR lanes per row (rows grid-strided over a fixed, SM-sized grid);
@@ -736,22 +706,6 @@ __global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ 
   scalar_op(op, S, state);
 }
 
-// S[slot] = sum of the block partials (fixed order, as k_reduce), then scalar op
-// `op` on one thread: one launch instead of two per CG scalar
-__global__ void k_reduce_step(int nparts, const double* __restrict__ part, double* __restrict__ S, int slot,
-                              int op, int* __restrict__ state) {
-  if (state[ST_STOP]) return;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
-  __shared__ double tmp[1];
-  block_sum_to(s, tmp);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    S[slot] = tmp[0];
-    scalar_op(op, S, state);
-  }
-}
-
 // device-side loop condition of the CUDA-graph WHILE node
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ state) {
   cudaGraphSetConditional(h, state[ST_STOP] ? 0u : 1u);
@@ -804,20 +758,6 @@ __global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__
   if (STOPPED) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = a[i];
-}
-
-__global__ void k_csr_warp_spmv(int nrows, const int64_t* __restrict__ ptr,
-                                const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                const double* __restrict__ x, double* __restrict__ y,
-                                const int* __restrict__ stop) {
-  if (STOPPED) return;
-  const int lane = threadIdx.x & 31;
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= nrows) return;
-  double s = 0.0;
-  for (int64_t k = ptr[row] + lane; k < ptr[row + 1]; k += 32) s += val[k] * x[idx[k]];
-  s = warp_sum(s);
-  if (lane == 0) y[row] = s;
 }
 
 }  // namespace dev

@@ -185,15 +185,8 @@ __global__ void k_front_finish_copy(PlanDev P, int g, const double* __restrict__
                                     double* __restrict__ umat);
 __global__ void k_front_fold_d(PlanDev P, int g, double* __restrict__ L, const double* __restrict__ dinv);
 
-// prolongation sum_i R_i^T x_i: out[e] = sum over the copies of dof e (fixed order)
-__global__ void k_prolong(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ pos,
-                          const double* __restrict__ x, double* __restrict__ out);
 
 // ---------------------------------------------------------- PCG pieces
-__global__ void k_spmv(int n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                       const double* __restrict__ val, const double* __restrict__ x,
-                       double* __restrict__ y, const double* __restrict__ dotw,
-                       double* __restrict__ part, const int* __restrict__ stop);
 // optional tail of a kernel that leaves one partial sum per block: the last block
 // to finish adds the partials in the order of k_reduce_step (same bits), stores
 // S[slot], runs the CG scalar step `op` and re-arms the counter (counter == null:
@@ -243,8 +236,6 @@ __global__ void k_dot_part(int n, const double* __restrict__ a, const double* __
 __global__ void k_reduce(int nparts, const double* __restrict__ part, double* __restrict__ out,
                          const int* __restrict__ stop);
 __global__ void k_scalar_step(int op, double* __restrict__ S, int* __restrict__ state);
-__global__ void k_reduce_step(int nparts, const double* __restrict__ part, double* __restrict__ S, int slot,
-                              int op, int* __restrict__ state);
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ state);
 __global__ void k_update_xr(int n, double* __restrict__ x, double* __restrict__ r,
                             const double* __restrict__ p, const double* __restrict__ q,
@@ -260,12 +251,6 @@ __global__ void k_combine3(int n, const double* __restrict__ a, const double* __
                            const int* __restrict__ stop);
 __global__ void k_copy(int n, const double* __restrict__ a, double* __restrict__ out,
                        const int* __restrict__ stop);
-
-// Z^T v and Z y over CSR copies of Z (rows = dofs) and Z^T (rows = coarse positions)
-__global__ void k_csr_warp_spmv(int nrows, const int64_t* __restrict__ ptr,
-                                const int32_t* __restrict__ idx, const double* __restrict__ val,
-                                const double* __restrict__ x, double* __restrict__ y,
-                                const int* __restrict__ stop);
 
 // scalar slots of the PCG state
 enum { S_RZ = 0, S_PQ, S_ALPHA, S_RR, S_NF, S_BETA, S_RZNEW, S_REL, S_TOL, S_TMP, S_COUNT };

@@ -2,7 +2,8 @@
 // nested-dissection ordering, elimination tree, postorder, column structures,
 // fundamental + relaxed supernodes, the level schedule, the extend-add
 // relative maps and the assembly map.  The numeric work (factorisation and the
-// triangular solves of the hot path) runs in CUDA kernels (factor.cu, trsv.cu).
+// triangular solves of the hot path) runs in CUDA kernels (kernels.cu: the
+// multifrontal factorisation, factor_driver.cu: its driver, sweep.cu: the sweeps).
 //
 // North star: "the local solves A_i^{-1} as supernodal sparse LDL^T factors
 // applied by hand-written level-scheduled triangular-solve kernels".
