@@ -323,7 +323,7 @@ def main():
                "ms_per_step": a_ms, "value": n * a_it / (a_ms / 1e3)}
         G.set_variant(args.variant)
 
-    info = G.info
+    info = G._info()   # after the solves: kernels per iteration, launches
     roof = roofline(G, sweep_ms, in_step, csweep_ms, cin_step, t_ms)
     # the whole PCG iteration against the same roofline: algorithmic bytes of one
     # iteration (MaxwellDD.bytes_model) x iterations / device time
