@@ -22,7 +22,9 @@ for p in range(nph):
     tot[k] = tot.get(k, 0) + span
     wait = np.median(tr[p, :, 2]) / 1e3
     tiles = np.median(tr[p, :, 3])
+    wmax = np.max(e - s) / 1e3
+    tmax = np.max(tr[p, :, 3])
     print(f"  {p:3d} {k:5s} [{ph[p,1]:8d},{ph[p,2]:8d}) start {s.min()/1e3:8.1f} end {e.max()/1e3:8.1f}"
-          f"  span {span:7.1f}  cta-median {work:6.1f} (tile-wait {wait:5.1f}, tiles {tiles:4.0f})"
-          f"  barrier-gap {gap:5.1f} us")
+          f"  span {span:7.1f}  cta-median {work:6.1f} max {wmax:6.1f} (tile-wait {wait:5.1f}, tiles {tiles:4.0f}"
+          f" max {tmax:4.0f})  barrier-gap {gap:5.1f} us")
 print("  totals:", {k: round(v, 1) for k, v in tot.items()})
