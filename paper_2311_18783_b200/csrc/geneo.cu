@@ -158,7 +158,7 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
         CUBLAS_CHECK(cublasDgeam(cb, CUBLAS_OP_T, CUBLAS_OP_N, g, n, &one, W1.p, n, &zero, Xt.p, g, Xt.p, g));
         CUSOLVER_CHECK(cusolverDnDpotrs(cs, CUBLAS_FILL_MODE_LOWER, g, n, Sg.p, g, Xt.p, g, info.p));
         CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, g, &mone, G.p, n, Xt.p, g, &one, P.p, n));
-        G.release(); W1.release(); Sg.release(); Xt.release();
+        W1.release(); Sg.release(); Xt.release();
       }
       dw.upload(Dw);
       dev::k_scale_rows<<<nb(n * n, 256), 256, 0, s>>>(n, n, dw.p, P.p);  // P <- D P
@@ -168,15 +168,55 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
       CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, n, n, n, &one, P.p, n, T1.p, n, &zero, Ad.p, n));
       T1.release();
       dev::k_symmetrize<<<nb(n * n, 256), 256, 0, s>>>(n, Ad.p);
+      // Deflation (reading R15): null(L) contains range(G_j) (P G_j = 0), so the
+      // eigenvectors with lambda > 0 are B-orthogonal to range(G_j).  B = A_j^Neu is
+      // near-singular exactly there (its gradients carry only gamma M energy:
+      // kappa(B) ~ 1e13 on c1), and a Cholesky-based reduction of the full pencil
+      // loses the eigenvalues near tau (c1 full size: 14.7 and 19.2 missing on
+      // subdomain 20).  The pencil is solved on {v : G_j^T B v = 0}, spanned by the
+      // last n - g columns Q2 of the QR factor Q of B G_j: (Q2^T L Q2, Q2^T B Q2),
+      // kappa ~ 1e7, the same nonzero eigenpairs; V = Q2 Y.
+      const bool deflate = g > 0 && !(getenv("MDD_GENEO_DEFLATE") && atoi(getenv("MDD_GENEO_DEFLATE")) == 0);
+      const int64_t ne = deflate ? n - g : n;
+      DBuf<double> Qf, Lc, Bc;
+      double* Lp = Ad.p;
+      double* Bp = Bd.p;
+      if (deflate) {
+        Qf.alloc(n * n);
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, g, n, &one, Bd.p, n, G.p, n, &zero, Qf.p, n));
+        DBuf<double> tq;
+        tq.alloc(g);
+        int lq = 0, lo = 0;
+        CUSOLVER_CHECK(cusolverDnDgeqrf_bufferSize(cs, n, g, Qf.p, n, &lq));
+        CUSOLVER_CHECK(cusolverDnDorgqr_bufferSize(cs, n, n, g, Qf.p, n, tq.p, &lo));
+        DBuf<double> wq;
+        wq.alloc(std::max(std::max(lq, lo), 1));
+        CUSOLVER_CHECK(cusolverDnDgeqrf(cs, n, g, Qf.p, n, tq.p, wq.p, std::max(lq, lo), info.p));
+        CUSOLVER_CHECK(cusolverDnDorgqr(cs, n, n, g, Qf.p, n, tq.p, wq.p, std::max(lq, lo), info.p));
+        const double* Q2 = Qf.p + (int64_t)g * n;
+        T1.alloc(n * ne);
+        Lc.alloc(ne * ne);
+        Bc.alloc(ne * ne);
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, ne, n, &one, Ad.p, n, Q2, n, &zero, T1.p, n));
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, ne, ne, n, &one, Q2, n, T1.p, n, &zero, Lc.p, ne));
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, ne, n, &one, Bd.p, n, Q2, n, &zero, T1.p, n));
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_T, CUBLAS_OP_N, ne, ne, n, &one, Q2, n, T1.p, n, &zero, Bc.p, ne));
+        T1.release();
+        dev::k_symmetrize<<<nb(ne * ne, 256), 256, 0, s>>>(ne, Lc.p);
+        dev::k_symmetrize<<<nb(ne * ne, 256), 256, 0, s>>>(ne, Bc.p);
+        Lp = Lc.p;
+        Bp = Bc.p;
+      }
+      G.release();
       lam.alloc(n);
       int lw = 0, meig = 0;
       const double vu = 1.0e300;
       CUSOLVER_CHECK(cusolverDnDsygvdx_bufferSize(cs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                                  CUSOLVER_EIG_RANGE_V, CUBLAS_FILL_MODE_LOWER, n, Ad.p, n,
-                                                  Bd.p, n, tau, vu, 0, 0, &meig, lam.p, &lw));
+                                                  CUSOLVER_EIG_RANGE_V, CUBLAS_FILL_MODE_LOWER, ne, Lp, ne,
+                                                  Bp, ne, tau, vu, 0, 0, &meig, lam.p, &lw));
       DBuf<double> work; work.alloc(std::max(lw, 1));
       CUSOLVER_CHECK(cusolverDnDsygvdx(cs, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUSOLVER_EIG_RANGE_V,
-                                       CUBLAS_FILL_MODE_LOWER, n, Ad.p, n, Bd.p, n, tau, vu, 0, 0, &meig,
+                                       CUBLAS_FILL_MODE_LOWER, ne, Lp, ne, Bp, ne, tau, vu, 0, 0, &meig,
                                        lam.p, work.p, lw, info.p));
       int hinfo = 0;
       CUDA_CHECK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -191,11 +231,19 @@ void geneo_all(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& out, 
         if (l[q] > tau) B.lambda.push_back(l[q]);
       B.k = (int)B.lambda.size();
       if (B.k > 0) {
-        // eigenvectors occupy the first meig columns of Ad, ascending eigenvalues
+        // eigenvectors occupy the first meig columns of Lp, ascending eigenvalues;
+        // deflated: V = Q2 Y first
         int first = meig - B.k;
+        const double* Y = Lp + (int64_t)first * ne;
+        DBuf<double> V;
+        if (deflate) {
+          V.alloc(n * B.k);
+          CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, B.k, ne, &one, Qf.p + (int64_t)g * n, n, Y, ne,
+                                   &zero, V.p, n));
+          Y = V.p;
+        }
         B.W.alloc(n * B.k);
-        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, B.k, n, &one, P.p, n, Ad.p + (int64_t)first * n,
-                                 n, &zero, B.W.p, n));
+        CUBLAS_CHECK(cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_N, n, B.k, n, &one, P.p, n, Y, n, &zero, B.W.p, n));
       }
       CUDA_CHECK(cudaStreamSynchronize(s));
     }

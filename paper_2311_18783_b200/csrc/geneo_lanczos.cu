@@ -295,28 +295,32 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
   LZ_CUBLAS(cublasSetStream(cb, s));
   LZ_CUSOLVER(cusolverDnSetStream(cs, s));
 
-  // ------------------------------------------- S_j = G^T A G, dense Cholesky
-  DBuf<double> Sd;
-  Sd.alloc((size_t)nsub * gpad * gpad);
-  Sd.zero(s);
-  k_gtag<<<nbk(NG, 128), 128, 0, s>>>(NG, gpad, npad, d_gj.p, d_gptr.p, d_gedge.p, d_gsgn.p, d_aptr.p, d_aidx.p,
-                                      d_aval.p, d_ecol.p, Sd.p);
-  CUDA_CHECK(cudaGetLastError());
-  {
+  // ---- S_j = G^T A G (for xi_0j) and S^B_j = G^T B G (the B-orthogonal deflation
+  // of range(G_j), reading R15), dense Cholesky factors
+  const bool deflate = !(getenv("MDD_GENEO_DEFLATE") && atoi(getenv("MDD_GENEO_DEFLATE")) == 0);
+  DBuf<double> Sd, SdB;
+  auto gram = [&](DBuf<double>& Sx, const double* vals, const char* what) {
+    Sx.alloc((size_t)nsub * gpad * gpad);
+    Sx.zero(s);
+    k_gtag<<<nbk(NG, 128), 128, 0, s>>>(NG, gpad, npad, d_gj.p, d_gptr.p, d_gedge.p, d_gsgn.p, d_aptr.p, d_aidx.p,
+                                        vals, d_ecol.p, Sx.p);
+    CUDA_CHECK(cudaGetLastError());
     int lw = 0;
-    LZ_CUSOLVER(cusolverDnDpotrf_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, gpad, Sd.p, gpad, &lw));
+    LZ_CUSOLVER(cusolverDnDpotrf_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, gpad, Sx.p, gpad, &lw));
     DBuf<double> work;
     work.alloc(std::max(lw, 1));
     DBuf<int> info;
     info.alloc(nsub);
     info.zero(s);
     for (int j = 0; j < nsub; ++j)
-      LZ_CUSOLVER(cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, gpad, Sd.p + (int64_t)j * gpad * gpad, gpad, work.p,
+      LZ_CUSOLVER(cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, gpad, Sx.p + (int64_t)j * gpad * gpad, gpad, work.p,
                                    lw, info.p + j));
     std::vector<int> hi = info.download();
     for (int j = 0; j < nsub; ++j)
-      MDD_REQUIRE(hi[j] == 0, 3, "G_j^T A_j G_j is not SPD in subdomain " + std::to_string(j));
-  }
+      MDD_REQUIRE(hi[j] == 0, 3, std::string(what) + " is not SPD in subdomain " + std::to_string(j));
+  };
+  gram(Sd, d_aval.p, "G_j^T A_j G_j");
+  if (deflate) gram(SdB, d_bval.p, "G_j^T A_j^Neu G_j");
 
   // ------------------------------------------- B_j^{-1}: supernodal LDL^T of A^Neu
   DevFactor neu;
@@ -353,9 +357,12 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
   DBuf<double> T1, T2, T3, Y, U, BU, Sn;
   T1.alloc(BLK); T2.alloc(BLK); T3.alloc(BLK); Y.alloc(BLK); U.alloc(BLK); BU.alloc(BLK);
   Sn.alloc((size_t)nsub * b * gpad);
-  Ptrs pSd, pSn;
+  Ptrs pSd, pSn, pSdB;
   pSd.set(Sd.p, (int64_t)gpad * gpad, nsub);
   pSn.set(Sn.p, (int64_t)b * gpad, nsub);
+  if (deflate) pSdB.set(SdB.p, (int64_t)gpad * gpad, nsub);
+  DBuf<double> ones;
+  ones.upload(std::vector<double>(NR, 1.0));
   const double one = 1.0, zero = 0.0, mone = -1.0;
   auto bd = [&](const double* val, const double* X, double* Yo, int nc) {
     k_bd_spmv<<<nbk(NR, 128), 128, 0, s>>>(NR, npad, npad, nc, d_aptr.p, d_aidx.p, val, X, Yo);
@@ -385,11 +392,24 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
     bd(d_aval.p, T1.p, T3.p, b);                      // A G s
     k_sub<<<nbk(n, 256), 256, 0, s>>>(n, T2.p, T3.p, Yo);
   };
+  // U <- U - G (G^T B G)^{-1} G^T B U: the B-orthogonal projection off range(G_j),
+  // where the wanted eigenvectors have no component and B^{-1} amplifies rounding
+  auto project = [&](double* Uo) {
+    if (!deflate) return;
+    bd(d_bval.p, Uo, T1.p, b);
+    k_gt<<<nbk(NG, 128), 128, 0, s>>>(NG, gpad, npad, b, d_gptr.p, d_gedge.p, d_gsgn.p, T1.p, Sn.p);
+    LZ_CUBLAS(cublasDtrsmBatched(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                 gpad, b, &one, pSdB.d.p, gpad, pSn.d.p, gpad, nsub));
+    LZ_CUBLAS(cublasDtrsmBatched(cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                 gpad, b, &one, pSdB.d.p, gpad, pSn.d.p, gpad, nsub));
+    k_g_apply<<<nbk(NR, 128), 128, 0, s>>>(NR, npad, gpad, b, d_ecol.p, Sn.p, Uo, ones.p, Uo);
+  };
   auto applyBinv = [&](const double* Yi, double* Uo) {
     for (int c = 0; c < b; ++c) {
       neu.sweep(Yi + (int64_t)c * npad, nullptr, s, nullptr);
       k_pos_scatter<<<nbk(ntot, 256), 256, 0, s>>>(ntot, d_pmap.p, neu.xb.p, Uo + (int64_t)c * npad);
     }
+    project(Uo);
   };
 
   // ------------------------------------------------------------ Lanczos
@@ -423,6 +443,7 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
                                  sB * sizeof(double), nsub, cudaMemcpyDeviceToDevice, s));
   };
   k_lz_random<<<nbk(BLK, 256), 256, 0, s>>>(BLK, npad, b, d_nj.p, U.p);
+  project(U.p);
   borth("start");
   store_block(0);
 

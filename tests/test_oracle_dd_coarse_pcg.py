@@ -288,3 +288,38 @@ def test_pcg_coarse_start_matches_dense_direct_solve():
     xd = np.linalg.solve(P.A.toarray(), f)
     assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
     assert hist[-1] <= 1e-12
+
+
+def test_geneo_pencil_deflation_keeps_the_kept_eigenpairs():
+    """Reading R15 (the device solves GEVP 3.5 on {v : G_j^T B v = 0}): null(L)
+    contains range(G_j) (P G_j = 0), so the eigenpairs with lambda > tau are
+    B-orthogonal to range(G_j) and the deflated pencil (Q2^T L Q2, Q2^T B Q2), Q2 the
+    last n - g columns of the QR factor of B G_j, has the same ones -- while its B
+    is far better conditioned."""
+    import scipy.linalg as sla
+    import workloads
+    from oracle import assembly, coarse, dd, mesh as om
+    w = workloads.make("c1", n=8, p=2)
+    m = om.mesh_of(w)
+    A, _, _ = assembly.system_matrix(m, w.mu_inv, w.eps, w.gamma)
+    C = assembly.gradient_matrix(m)
+    dec = dd.decompose(m, w.px, w.py, w.pz, w.overlap)
+    Aneu = dd.neumann_matrices(m, w.mu_inv, w.eps, w.gamma, dec)
+    tau = 1.0 / w.threshold
+    for i in (0, 3):
+        d = dec.dofs[i]
+        cols, Gi = coarse.local_gradient_basis(C, d)
+        lam, V, _ = coarse.geneo_local(A[d][:, d].tocsr(), Aneu[i], dec.pou[i], Gi, tau)
+        Ad, B, G = A[d][:, d].toarray(), Aneu[i].toarray(), Gi.toarray()
+        P = np.eye(len(d)) - coarse.xi_projection(Ad, G)
+        DP = dec.pou[i][:, None] * P
+        L = DP.T @ Ad @ DP
+        L = 0.5 * (L + L.T)
+        assert np.abs(L @ G).max() <= 1e-9 * np.abs(L).max()          # range(G) in null(L)
+        assert np.abs(G.T @ B @ V).max() <= 1e-8 * np.abs(B @ V).max()  # kept V B-orthogonal to it
+        Q, _ = sla.qr(B @ G, mode="full")
+        Q2 = Q[:, G.shape[1]:]
+        Lc, Bc = Q2.T @ L @ Q2, Q2.T @ B @ Q2
+        lc = sla.eigh(0.5 * (Lc + Lc.T), 0.5 * (Bc + Bc.T), eigvals_only=True, subset_by_value=(tau, np.inf))
+        assert len(lc) == len(lam) and np.allclose(lc, lam, rtol=1e-8, atol=0)
+        assert np.linalg.cond(Bc) < 1e-3 * np.linalg.cond(B)
