@@ -76,10 +76,13 @@ __device__ __forceinline__ double gather_t(const SweepDev& S, long long q) {
   for (i64 k = S.cptr[q]; k < S.cptr[q + 1]; ++k) v += __ldcg(S.upd + S.cidx[k]);
   return v;
 }
-// one row of the backward task vector: w = [D z_c ; -x_off]
+// one row of the backward task vector: w = [D z_c ; -x_off]; a pivot dropped by
+// the rank-revealing factorisation has D^{-1} = 0 and z_c = 0: its D z_c is 0
 __device__ __forceinline__ double gather_w(const SweepDev& S, long long q) {
   const i64 w = S.wsrc[q];
-  return w >= 0 ? __ldcg(S.xf + w) / __ldg(S.dinv + w) : -__ldcg(S.xb + (-w - 1));
+  if (w < 0) return -__ldcg(S.xb + (-w - 1));
+  const double di = __ldg(S.dinv + w);
+  return di != 0.0 ? __ldcg(S.xf + w) / di : 0.0;
 }
 
 // grid-wide barrier over co-resident CTAs (cumulative counter, no reset)
