@@ -110,7 +110,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       // a task's vector (up to kGroup row blocks / column blocks) must fit a
       // kVecMax shared-memory slot: RB, CB <= kVecMax / kGroup
       const int CB = std::min(nc, env_cb);
-      const int RB = std::max(1, std::min(dev::kVecMax / 4, dev::kTileMax / CB));
+      // an odd row count keeps the column-strided reads of the forward 2-D tiles
+      // (lanes down the columns, stride RB) free of shared-memory bank conflicts
+      int RB = std::max(1, std::min(dev::kVecMax / 4, dev::kTileMax / CB));
+      if (RB > 1 && !(RB & 1)) --RB;
       const int nrb = (nr + RB - 1) / RB, ncb = (nc + CB - 1) / CB;
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;   // sized for groups of one tile

@@ -270,6 +270,34 @@ __device__ __forceinline__ void tile_matvec_t_w(const double* T, int R, int C, c
     }
   }
 }
+// Forward 2-D tile, rows in groups of 8 per warp (warp w: rows 8w.. and 64+8w..),
+// lanes down the columns with 8 row partials each, then warp_reduce8: every lane
+// ends with the full sum of row r0 + (lane >> 2), added to its register
+// accumulator -- no shared-memory reduction and no block barrier inside the tile,
+// so the partial sums of a group of tiles stay in registers.  Fixed order.
+__device__ __forceinline__ void tile_rows8(const double* T, int R, int C, const double* v, double& acc0,
+                                           double& acc1) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int gi = 0; gi < 2; ++gi) {
+    const int r0 = 8 * (warp + 8 * gi);
+    if (r0 >= R) break;  // warp-uniform
+    double p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = 0.0;
+    for (int c = lane; c < C; c += 32) {
+      const double vc = v[c];
+      const double* col = T + c * R + r0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (r0 + k < R) p[k] += col[k] * vc;
+    }
+    const double sm8 = warp_reduce8(p, lane);
+    if (gi == 0) acc0 += sm8;
+    else acc1 += sm8;
+  }
+}
+
 // groups of 8 columns for wide tiles (2-D: 64 columns), of 4 for narrow ones
 template <class Fin>
 __device__ __forceinline__ void tile_matvec_t(const double* T, int R, int C, const double* w, double* red,
@@ -401,7 +429,11 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ __align__(16) MTaskDesc s_desc[kDescRing];
   __shared__ int s_tinfo[kStages];
-  __shared__ int s_flag;
+  // 2-D task groups whose combine is deferred to the end of the phase (or until the
+  // list is full): the task, and whether its atomic made it the last of its block
+  constexpr int kMaxPend = 32;
+  __shared__ int s_pend_task[kMaxPend];
+  __shared__ unsigned char s_pend_last[kMaxPend];
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
@@ -506,6 +538,61 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       };
       if (tid == 0)
         for (int q = 0; q < kStages; ++q) issue_next();
+      // last group of its row block (fwd) / column block (bwd): combine the ntl
+      // partials, Lq lanes per output (lane s sums partials s, s+Lq, ..., then a
+      // shuffle tree): a fixed order that depends on ntl only
+      auto combine = [&](const MTaskDesc& D) {
+        const int m = fwd ? D.rows : D.cols;
+        const int Lq = m <= 32 ? 8 : m <= 64 ? 4 : m <= 128 ? 2 : 1;
+        const double* pb = fwd ? S.fpart + D.comb : S.bpart + D.comb;
+        const i64 ld = fwd ? D.nr : D.nc;
+        const int sub = tid & (Lq - 1);
+        for (int o0 = 0; o0 < m; o0 += kSweepThreads / Lq) {
+          const int o = o0 + tid / Lq;
+          double s0 = 0.0, s1 = 0.0;
+          if (o < m) {
+            int q = sub;
+            for (; q + Lq < D.ntl; q += 2 * Lq) {
+              s0 += __ldcg(pb + (i64)q * ld + o);
+              s1 += __ldcg(pb + (i64)(q + Lq) * ld + o);
+            }
+            if (q < D.ntl) s0 += __ldcg(pb + (i64)q * ld + o);
+          }
+          double sum = s0 + s1;
+          for (int w = 1; w < Lq; w <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, w);
+          if (o < m && sub == 0) {
+            if (fwd) {
+              const int r = D.rb * D.RB + o;
+              if (r < D.nc) S.xf[D.col0 + r] = sum;
+              else S.upd[D.uptr + (r - D.nc)] = (fused ? gather_t(S, D.vo + r) : __ldcg(S.vb + D.vo + r)) - sum;
+            } else {
+              S.xb[D.col0 + D.cb * D.CB + o] = sum;
+            }
+          }
+        }
+      };
+      // The atomic that publishes a group's partials is issued by thread 32 and its
+      // result is only read at the next group's atomic or at the flush: its round
+      // trip to L2 overlaps the next task instead of stalling the CTA at a barrier
+      // (the stall ncu put at 15 % of the coarse sweep's samples).  The combines run
+      // at the flush: their outputs are read only by later phases.
+      int npend = 0;                               // uniform
+      unsigned long long infl_old = 0;             // thread 32: the in-flight atomic
+      int infl_slot = -1, infl_ntl = 0;
+      auto flush = [&]() {
+        if (tid == 32 && infl_slot >= 0) {
+          s_pend_last[infl_slot] = infl_old + 1 == cur * (unsigned long long)infl_ntl;
+          infl_slot = -1;
+        }
+        __syncthreads();
+        for (int q = 0; q < npend; ++q)
+          if (s_pend_last[q]) {
+            const MTaskDesc Dp = MT[task_of(s_pend_task[q])];
+            combine(Dp);
+          }
+        __syncthreads();
+        npend = 0;
+      };
       int cs = 0;  // tiles consumed in this phase
       for (int i = 0;; ++i) {
         const int k = task_of(i);
@@ -605,14 +692,14 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           // ---------------- a group of <= 4 tiles of a 2-D supernode: one row block and
           // consecutive column blocks (fwd) / one column block and consecutive row
           // blocks (bwd), accumulated in shared memory into one partial sum
+          double acc0 = 0.0, acc1 = 0.0;  // forward: this lane's rows (tile_rows8)
           for (int kk = D.k0; kk < D.k1; ++kk) {
             const int j = kk - D.k0;
             next_tile_and_wait(kk);
             const double* T = sm + buf * kTileMax;
             if (fwd) {
               const int cols = min(D.CB, D.nc - (D.cb + j) * D.CB);
-              if (j == 0) tile_matvec(T, D.rows, cols, vv, red, [&](int r, double y) { vec2[r] = y; });
-              else tile_matvec(T, D.rows, cols, vv + j * D.CB, red, [&](int r, double y) { vec2[r] += y; });
+              tile_rows8(T, D.rows, cols, vv + j * D.CB, acc0, acc1);
             } else {
               const int rows = min(D.RB, D.nr - (D.rb + j) * D.RB);
               if (j == 0) tile_matvec_t(T, rows, D.cols, vv, red, [&](int c, double y) { vec2[c] = y; });
@@ -621,57 +708,34 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             __syncthreads();
             tile_done();
           }
-          {
-            double* const part = (fwd ? S.fpart : S.bpart) + D.part;
-            const int m = fwd ? D.rows : D.cols;
-            for (int q = tid; q < m; q += kSweepThreads) part[q] = vec2[q];
-          }
-          __syncthreads();
-          if (tid == 0) {
-            // one acq_rel atomic publishes this group's partial sums and tells the
-            // last group of the row / column block to combine
-            unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
-            unsigned long long old;
-            asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(c) : "memory");
-            s_flag = old + 1 == cur * (unsigned long long)D.ntl;
-          }
-          __syncthreads();
-          if (s_flag) {
-            // last group of its row block (fwd) / column block (bwd): combine the
-            // ntl partials, Lq lanes per output (lane s sums partials s, s+Lq, ...,
-            // then a shuffle tree): a fixed order that depends on ntl only
-            const int m = fwd ? D.rows : D.cols;
-            const int Lq = m <= 32 ? 8 : m <= 64 ? 4 : m <= 128 ? 2 : 1;
-            const double* pb = fwd ? S.fpart + D.comb : S.bpart + D.comb;
-            const i64 ld = fwd ? D.nr : D.nc;
-            const int sub = tid & (Lq - 1);
-            for (int o0 = 0; o0 < m; o0 += kSweepThreads / Lq) {
-              const int o = o0 + tid / Lq;
-              double s0 = 0.0, s1 = 0.0;
-              if (o < m) {
-                int q = sub;
-                for (; q + Lq < D.ntl; q += 2 * Lq) {
-                  s0 += __ldcg(pb + (i64)q * ld + o);
-                  s1 += __ldcg(pb + (i64)(q + Lq) * ld + o);
-                }
-                if (q < D.ntl) s0 += __ldcg(pb + (i64)q * ld + o);
-              }
-              double sum = s0 + s1;
-              for (int w = 1; w < Lq; w <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, w);
-              if (o < m && sub == 0) {
-                if (fwd) {
-                  const int r = D.rb * D.RB + o;
-                  if (r < D.nc) S.xf[D.col0 + r] = sum;
-                  else S.upd[D.uptr + (r - D.nc)] = (fused ? gather_t(S, D.vo + r) : __ldcg(S.vb + D.vo + r)) - sum;
-                } else {
-                  S.xb[D.col0 + D.cb * D.CB + o] = sum;
-                }
-              }
+          if (fwd) {
+            double* const part = S.fpart + D.part;
+            const int lane = tid & 31, r = 8 * (tid >> 5) + (lane >> 2);
+            if ((lane & 3) == 0) {
+              if (r < D.rows) part[r] = acc0;
+              if (r + 64 < D.rows) part[r + 64] = acc1;
             }
+          } else {
+            double* const part = S.bpart + D.part;
+            for (int q = tid; q < D.cols; q += kSweepThreads) part[q] = vec2[q];
           }
+          __syncthreads();
+          if (tid == 32) {
+            // one acq_rel atomic publishes this group's partial sums (ordered after the
+            // CTA's part[] writes by the bar.sync above) and tells the last group of
+            // the row / column block to combine
+            if (infl_slot >= 0) s_pend_last[infl_slot] = infl_old + 1 == cur * (unsigned long long)infl_ntl;
+            unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
+            asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(infl_old) : "l"(c) : "memory");
+            infl_ntl = D.ntl;
+            infl_slot = npend;
+            s_pend_task[npend] = i;
+          }
+          if (++npend == kMaxPend) flush();
         }
         __syncthreads();
       }
+      if (npend > 0) flush();
     }
     // the next phases read vb / upd / xf / xb with TMA bulk copies (async proxy):
     // order this thread's generic-proxy global writes before them
