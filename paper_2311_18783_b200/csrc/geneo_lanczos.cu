@@ -184,19 +184,6 @@ __global__ void k_gtag(int64_t nnodes, int gpad, int npad, const int* __restrict
   }
 }
 
-// A_j <- (A_j + A_j^T) / 2 for the m x m (ld m) matrices at stride `stride`
-__global__ void k_sym_batched(int nsub, int m, int64_t stride, double* __restrict__ A) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (int64_t)nsub * m * m) return;
-  const int64_t j = q / ((int64_t)m * m), e = q % ((int64_t)m * m);
-  const int r = (int)(e % m), c = (int)(e / m);
-  if (r <= c) return;
-  double* Aj = A + j * stride;
-  const double v = 0.5 * (Aj[(int64_t)c * m + r] + Aj[(int64_t)r * m + c]);
-  Aj[(int64_t)c * m + r] = v;
-  Aj[(int64_t)r * m + c] = v;
-}
-
 struct Ptrs {
   DBuf<double*> d;
   void set(double* base, int64_t stride, int n) {
@@ -428,9 +415,8 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
   // ------------------------------------------------------------ Lanczos
   DBuf<double> Q, T, H, Cb, Tw, w;
   Q.alloc((size_t)nsub * mmax * npad);
-  // L Q_k of every block (the Rayleigh-Ritz matrix Q^T L Q is formed from them)
-  DBuf<double> LQ;
-  LQ.alloc((size_t)nsub * mmax * npad);
+  T.alloc((size_t)nsub * mmax * mmax);
+  T.zero(s);
   H.alloc((size_t)nsub * mmax * b);
   Cb.alloc((size_t)nsub * b * b);
   Ptrs pCb, pU;
@@ -461,17 +447,6 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
   borth("start");
   store_block(0);
 
-  // The Rayleigh-Ritz matrix of the current basis, Q^T L Q (B-orthonormal Q), formed
-  // exactly from the stored L Q blocks rather than from the three-term recurrence:
-  // its Ritz values interlace the true eigenvalues (theta_k <= lambda_k), so the
-  // count above tau can only approach the true count from below.  The recurrence's
-  // block tridiagonal T assumed an exact B^{-1}; with kappa(A_j^Neu) ~ 1e13 it gave
-  // spurious Ritz values near tau (c1 full size: 2336 GenEO vectors vs 2073).
-  auto rayleigh_ritz = [&](int m) {
-    LZ_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_T, CUBLAS_OP_N, m, m, npad, &one, Q.p, npad, sQ, LQ.p, npad, sQ,
-                                        &zero, Tw.p, m, (int64_t)mmax * mmax, nsub));
-    k_sym_batched<<<nbk((int64_t)nsub * m * m, 256), 256, 0, s>>>(nsub, m, (int64_t)mmax * mmax, Tw.p);
-  };
   const double rtol = 1e-10;
   std::vector<int> prev_cnt(nsub, -1), done(nsub, 0), kcnt(nsub, 0);
   std::vector<std::vector<double>> lam(nsub);
@@ -493,8 +468,7 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
     // A_k = Q_k^T L Q_k (b x b), symmetrised into T(k, k)
     LZ_CUBLAS(cublasDgemmStridedBatched(cb, CUBLAS_OP_T, CUBLAS_OP_N, b, b, npad, &one, Qk, npad, sQ, Y.p, npad, sB,
                                         &zero, Cb.p, b, (int64_t)b * b, nsub));
-    CUDA_CHECK(cudaMemcpy2DAsync(LQ.p + (int64_t)k * b * npad, sQ * sizeof(double), Y.p, sB * sizeof(double),
-                                 sB * sizeof(double), nsub, cudaMemcpyDeviceToDevice, s));
+    k_put_block<<<nbk(nsub * b * b, 128), 128, 0, s>>>(nsub, b, mmax, T.p, k * b, k * b, Cb.p, 0, 0, 1);
     applyBinv(Y.p, U.p);
     if (m >= mmax) {
       mfinal = m;
@@ -511,16 +485,18 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
     borth("step");
     store_block(k + 1);
     // T(k+1, k) = R (upper triangular), T(k, k+1) = R^T
+    k_put_block<<<nbk(nsub * b * b, 128), 128, 0, s>>>(nsub, b, mmax, T.p, (k + 1) * b, k * b, Cb.p, 1, 1, 0);
     if (m < next_check && m + b < mmax) continue;
     next_check = std::min(mmax, std::max(next_check + 2 * b, (next_check * 3) / 2) / b * b);
     // ---- checkpoint: Ritz values and residual bounds ||R s_i(last block)||
     int lw = 0;
-    rayleigh_ritz(m);
     LZ_CUSOLVER(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, Tw.p, m, w.p, &lw));
     if (lw > lwork_max) { lwork_max = lw; work.alloc(lw); }
     for (int j = 0; j < nsub; ++j) {
       if (done[j]) continue;
       double* Twj = Tw.p + (int64_t)j * mmax * mmax;
+      CUDA_CHECK(cudaMemcpy2DAsync(Twj, m * sizeof(double), T.p + (int64_t)j * mmax * mmax, mmax * sizeof(double),
+                                   m * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
       LZ_CUSOLVER(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, Twj, m,
                                    w.p + (int64_t)j * mmax, work.p, lw, einfo.p + j));
     }
@@ -587,11 +563,12 @@ void geneo_lanczos(const GeneoInputs& in, double tau, std::vector<GeneoBlock>& o
   {
     const int m = mfinal;
     int lw = 0;
-    rayleigh_ritz(m);
     LZ_CUSOLVER(cusolverDnDsyevd_bufferSize(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, Tw.p, m, w.p, &lw));
     if (lw > lwork_max) { lwork_max = lw; work.alloc(lw); }
     for (int j = 0; j < nsub; ++j) {
       double* Twj = Tw.p + (int64_t)j * mmax * mmax;
+      CUDA_CHECK(cudaMemcpy2DAsync(Twj, m * sizeof(double), T.p + (int64_t)j * mmax * mmax, mmax * sizeof(double),
+                                   m * sizeof(double), m, cudaMemcpyDeviceToDevice, s));
       LZ_CUSOLVER(cusolverDnDsyevd(cs, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, m, Twj, m,
                                    w.p + (int64_t)j * mmax, work.p, lw, einfo.p + j));
     }
