@@ -331,6 +331,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         X.k0 = (int)td.size();
         for (int t : c.tiles) push_td(t);
         X.k1 = (int)td.size();
+        for (int q = 0; q < dev::kTdInline && X.k0 + q < X.k1; ++q) X.td[q] = td[X.k0 + q];
         out.push_back(X);
       }
     }

@@ -100,9 +100,11 @@ constexpr int kStages = 2;       // tile ring slots per CTA (one tile streams wh
 constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can span)
 constexpr int kDescAhead = 4;    // M-task descriptors streamed ahead of the current task
 constexpr int kDescRing = 8;     // descriptor ring slots (> kDescAhead)
-// MDD_SWEEP_TRACE words per (phase, CTA): start, end (%globaltimer, thread 0),
-// time thread 0 waited on tile mbarriers, tiles consumed
-constexpr int kTraceWords = 4;
+// MDD_SWEEP_TRACE words per (phase, CTA), thread 0's view (%globaltimer ns): start,
+// end, time waiting on tile mbarriers, tiles consumed, time in the deferred-combine
+// flushes, time from a task's top to its first tile wait (descriptor ring + fused
+// gather), time from a tile's arrival to its slot refill (compute + barrier), tasks
+constexpr int kTraceWords = 8;
 constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
 
 // one task of an M phase (factor_driver.cu builds them, forward and backward)
@@ -120,7 +122,14 @@ struct __align__(16) MTaskDesc {
   int voff;         // offset of the vector inside its shared-memory buffer
   int vbytes;       // bytes of the vector bulk copy
   int vn;           // rows of the task vector (vb rows [vlo2 + voff, + vn))
+  int pad_[3];
+  // the task's first kTdInline tile descriptors (tdesc[k0 ..]): the producer thread
+  // issues their bulk copies from shared memory, with no dependent global load on
+  // the CTA's critical path (every task has <= 4 tiles at the default knobs)
+  int4 td[4];
 };
+constexpr int kTdInline = 4;
+static_assert(sizeof(MTaskDesc) == 192, "MTaskDesc layout");
 
 struct SweepDev {
   PlanDev P;

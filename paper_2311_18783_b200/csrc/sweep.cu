@@ -452,7 +452,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     const int4 PH = S.phases[ph];
     const int kind = PH.x;
     const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
-    unsigned long long t_wait = 0, t_tiles = 0;  // trace: thread 0's time in tile waits, tiles
+    // trace (thread 0): time in tile waits, tiles, flushes, task starts, tile bodies, tasks
+    unsigned long long t_wait = 0, t_tiles = 0, t_flush = 0, t_start = 0, t_body = 0, t_tasks = 0;
+    const bool trc = S.trace && tid == 0;
     if (kind == PH_GF) {
       // t = [b_c ; 0] + children's updates, one row per thread
       for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_t(S, q);
@@ -478,10 +480,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         const int k = (i & 1) ? i * G + (G - 1 - b) : i * G + b;
         return k < ntk ? k : -1;
       };
-      // thread 0: stream tdesc[kk] into ring slot `bf`, plus (vbytes > 0) the task
+      // thread 0: stream the tile of descriptor d into ring slot `bf`, plus (vbytes > 0) the task
       // vector into vector slot `vs`
-      auto prefetch = [&](int kk, int bf, long long vlo2, int vbytes, int vs) {
-        const int4 d = S.tdesc[kk];
+      auto prefetch = [&](const int4 d, int bf, long long vlo2, int vbytes, int vs) {
         s_tinfo[bf] = d.x;  // read by the consumer after at least one __syncthreads
         const int64_t off = (int64_t)(((uint64_t)(uint32_t)d.w << 32) | (uint32_t)d.z);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[bf])),
@@ -532,7 +533,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         }
         const MTaskDesc& Dp = s_desc[pi % kDescRing];
         const bool first = pk == Dp.k0;
-        prefetch(pk, ps % kStages, Dp.vlo2, first && !fused ? Dp.vbytes : 0, pi % kVecSlots);
+        const int j = pk - Dp.k0;
+        prefetch(j < kTdInline ? Dp.td[j] : S.tdesc[pk], ps % kStages, Dp.vlo2, first && !fused ? Dp.vbytes : 0,
+                 pi % kVecSlots);
         ++ps;
         ++pk;
       };
@@ -580,6 +583,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       unsigned long long infl_old = 0;             // thread 32: the in-flight atomic
       int infl_slot = -1, infl_ntl = 0;
       auto flush = [&]() {
+        const unsigned long long f0 = trc ? globaltimer() : 0ull;
         if (tid == 32 && infl_slot >= 0) {
           s_pend_last[infl_slot] = infl_old + 1 == cur * (unsigned long long)infl_ntl;
           infl_slot = -1;
@@ -592,11 +596,14 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           }
         __syncthreads();
         npend = 0;
+        if (trc) t_flush += globaltimer() - f0;
       };
       int cs = 0;  // tiles consumed in this phase
       for (int i = 0;; ++i) {
         const int k = task_of(i);
         if (k < 0) break;
+        const unsigned long long s0 = trc ? globaltimer() : 0ull;
+        if (trc) ++t_tasks;
         // descriptors i+1, i+2 must be resident before the cursor reaches them;
         // task i+3's starts streaming now
         desc_fetch(i + kDescAhead);
@@ -620,17 +627,20 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           __syncthreads();
         }
         int buf = 0;
+        if (trc) t_start += globaltimer() - s0;
+        unsigned long long b0 = 0;
         // wait for the next tile of the stream (its ring slot becomes `buf`)
         auto next_tile_and_wait = [&](int) {
           buf = cs % kStages;
-          const unsigned long long w0 = (S.trace && tid == 0) ? globaltimer() : 0ull;
+          const unsigned long long w0 = trc ? globaltimer() : 0ull;
           mbar_wait(&mbar[buf], (parbits >> buf) & 1u);
-          if (S.trace && tid == 0) { t_wait += globaltimer() - w0; ++t_tiles; }
+          if (trc) { b0 = globaltimer(); t_wait += b0 - w0; ++t_tiles; }
           parbits ^= 1u << buf;
         };
         // after the tile's last read (callers __syncthreads first): refill its slot
         auto tile_done = [&]() {
           if (tid == 0) issue_next();
+          if (trc) t_body += globaltimer() - b0;
           ++cs;
         };
 #ifdef MDD_DEBUG_NOCOMPUTE
@@ -740,12 +750,16 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     // the next phases read vb / upd / xf / xb with TMA bulk copies (async proxy):
     // order this thread's generic-proxy global writes before them
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (S.trace && tid == 0) {
+    if (trc) {
       unsigned long long* tr = S.trace + kTraceWords * ((size_t)ph * gridDim.x + blockIdx.x);
       tr[0] = t_ph;
       tr[1] = globaltimer();
       tr[2] = t_wait;
       tr[3] = t_tiles;
+      tr[4] = t_flush;
+      tr[5] = t_start;
+      tr[6] = t_body;
+      tr[7] = t_tasks;
     }
     if (ph + 1 < S.nphases)
       grid_barrier(S.ctl, ((cur - 1) * (unsigned long long)(S.nphases - 1) + ph + 1) * grid);

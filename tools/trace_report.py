@@ -24,7 +24,14 @@ for p in range(nph):
     tiles = np.median(tr[p, :, 3])
     wmax = np.max(e - s) / 1e3
     tmax = np.max(tr[p, :, 3])
-    print(f"  {p:3d} {k:5s} [{ph[p,1]:8d},{ph[p,2]:8d}) start {s.min()/1e3:8.1f} end {e.max()/1e3:8.1f}"
+    extra = ""
+    if words >= 8:
+        fl, st, bo = (float(np.median(tr[p, :, q])) / 1e3 for q in (4, 5, 6))
+        nt = np.median(tr[p, :, 7])
+        extra = f" flush {fl:6.1f} task-start {st:6.1f} tile-body {bo:6.1f} tasks {nt:4.0f}"
+        for key, v in (("flush", fl), ("task-start", st), ("tile-body", bo), ("tile-wait", wait)):
+            tot[key] = tot.get(key, 0) + v
+    print(f"  {p:3d} {k:5s} [{ph[p,1]:8d},{ph[p,2]:8d})"
           f"  span {span:7.1f}  cta-median {work:6.1f} max {wmax:6.1f} (tile-wait {wait:5.1f}, tiles {tiles:4.0f}"
-          f" max {tmax:4.0f})  barrier-gap {gap:5.1f} us")
+          f" max {tmax:4.0f}){extra}  barrier-gap {gap:5.1f} us")
 print("  totals:", {k: round(v, 1) for k, v in tot.items()})
