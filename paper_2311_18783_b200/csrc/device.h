@@ -78,11 +78,12 @@ struct DevFactor {
   // persistent level-synchronous sweep (sweep.cu)
   DBuf<int4> phases, tdesc, tiles;
   DBuf<dev::MTaskDesc> mt_f, mt_b;
+  DBuf<dev::CombDesc> cmb;
   DBuf<int64_t> tile_off, sn_fpart, sn_bpart, vb_off, cptr, cidx, wsrc;
-  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb, sn_rbc, sn_cbc;
+  DBuf<int> sn_RB, sn_CB, sn_nrb, sn_ncb;
   DBuf<int32_t> gsrc;
   DBuf<double> Lt, fpart, bpart, vb;
-  DBuf<unsigned long long> rb_cnt, cb_cnt, ctl, trace;
+  DBuf<unsigned long long> ctl, trace;
   int nphases = 0, ntiles = 0, sweep_grid = 0, n_out = 0;
   // plan statistics (mdd_info): supernodes swept as packed / strip / 2-D tasks,
   // fronts factorised by the blocked (cuBLAS trailing update) path

@@ -65,7 +65,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   // tiles[] = {g, a, b, kind}: kind 0 = 2-D (a = rb, b = cb), 1 = forward strip
   // (a = first row), 2 = backward strip (b = first column), 3 = small column tile
   const int nsn = fp.nsn;
-  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn, 1), vncb(nsn, 1), vrbc(nsn, 0), vcbc(nsn, 0);
+  std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn, 1), vncb(nsn, 1);
   std::vector<uint8_t> mode(nsn);  // 0 small, 1 strip, 2 2-D
   std::vector<int64_t> vfp(nsn, 0), vbp(nsn, 0);
   std::vector<std::vector<int>> ft(nsn), bt(nsn);  // forward / backward tiles (2-D: same list)
@@ -73,7 +73,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   std::vector<int2> rc;  // rows x cols of each tile
   std::vector<int64_t> toff;
   int64_t off = 0, nfp = 0, nbp = 0;
-  int nrbc = 0, ncbc = 0;
   auto add_tile = [&](int4 t, int rows, int cols) {
     tl.push_back(t);
     rc.push_back(make_int2(rows, cols));
@@ -118,8 +117,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       vRB[g] = RB; vCB[g] = CB; vnrb[g] = nrb; vncb[g] = ncb;
       vfp[g] = nfp; nfp += (int64_t)ncb * nr;   // sized for groups of one tile
       vbp[g] = nbp; nbp += (int64_t)nrb * nc;
-      vrbc[g] = nrbc; nrbc += nrb;
-      vcbc[g] = ncbc; ncbc += ncb;
       for (int rb = 0; rb < nrb; ++rb) {
         const int rend = std::min(nr, (rb + 1) * RB), rows = rend - rb * RB;
         for (int cb = 0; cb < ncb && cb * CB < rend; ++cb)
@@ -175,6 +172,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   std::vector<dev::MTaskDesc> mtf, mtb;
   std::vector<int4> td;
   std::vector<int> lev_f(fp.nlevels + 1, 0), lev_b(fp.nlevels + 1, 0);
+  // combine items (one per row block / column block of a 2-D supernode) per level
+  std::vector<dev::CombDesc> cm;
+  std::vector<int> cmf(fp.nlevels + 1, 0), cmb_lev(fp.nlevels + 1, 0);
   auto push_td = [&](int t) {
     // .x: tile id, or for packed small tiles first column | columns << 16 (the kernel
     // needs them per tile)
@@ -269,7 +269,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
                 X.rows = rend - rb * RB;
                 X.part = vfp[g] + (int64_t)ch * nr + (int64_t)rb * RB;
                 X.comb = vfp[g] + (int64_t)rb * RB;
-                X.cnt = vrbc[g] + rb;
                 X.ntl = nch;
                 set_vec(X, vvo[g] + (int64_t)X.cb * CB, vvo[g] + std::min<int64_t>(nc, (int64_t)cend * CB));
                 Cand c{0, X, {}};
@@ -290,7 +289,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
                 X.cols = std::min(CB, nc - cb * CB);
                 X.part = vbp[g] + (int64_t)ch * nc + (int64_t)cb * CB;
                 X.comb = vbp[g] + (int64_t)cb * CB;
-                X.cnt = vcbc[g] + cb;
                 X.ntl = nch;
                 set_vec(X, vvo[g] + (int64_t)X.rb * RB, vvo[g] + std::min<int64_t>(nr, (int64_t)rend_b * RB));
                 Cand c{0, X, {}};
@@ -326,6 +324,23 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         if (mk < best) { best = mk; lt.swap(c); }
         if (getenv("MDD_FIXED_GROUP")) break;  // debug: always groups of 4
       }
+      if (dir == 0) cmf[l] = (int)cm.size(); else cmb_lev[l] = (int)cm.size();
+      for (auto& c : lt) {
+        const dev::MTaskDesc& X0 = c.d;
+        if (X0.big == 1 && X0.part == X0.comb) {  // first chunk of its row / column block
+          dev::CombDesc C{};
+          C.comb = X0.comb;
+          C.col0 = X0.col0;
+          C.uptr = X0.uptr;
+          C.vo = X0.vo;
+          C.ld = dir == 0 ? X0.nr : X0.nc;
+          C.ntl = X0.ntl;
+          C.m = dir == 0 ? X0.rows : X0.cols;
+          C.first = dir == 0 ? X0.rb * X0.RB : X0.cb * X0.CB;
+          C.nc = X0.nc;
+          cm.push_back(C);
+        }
+      }
       for (auto& c : lt) {
         dev::MTaskDesc X = c.d;
         X.k0 = (int)td.size();
@@ -336,6 +351,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       }
     }
     lev[fp.nlevels] = (int)out.size();
+    if (dir == 0) cmf[fp.nlevels] = (int)cm.size(); else cmb_lev[fp.nlevels] = (int)cm.size();
   }
   // levels with few tasks per CTA gather their task vectors inside the tasks (no
   // flat G phase and no grid barrier before them); the leaf levels keep the
@@ -349,11 +365,14 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     const bool fz = fused(lev_f, l);
     if (!fz) ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], fz ? 1 : 0));
+    // the level's 2-D partial sums, added before any later phase reads xf / upd
+    if (cmf[l + 1] > cmf[l]) ph.push_back(make_int4(dev::PH_CF, cmf[l], cmf[l + 1], fz ? 1 : 0));
   }
   for (int l = fp.nlevels - 1; l >= 0; --l) {
     const bool fz = fused(lev_b, l);
     if (!fz) ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], fz ? 1 : 0));
+    if (cmb_lev[l + 1] > cmb_lev[l]) ph.push_back(make_int4(dev::PH_CB, cmb_lev[l], cmb_lev[l + 1], 0));
   }
   if (prolong_n > 0) {
     ph.push_back(make_int4(dev::PH_PR, 0, prolong_n, 0));
@@ -366,11 +385,11 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   phases.upload(ph);
   mt_f.upload(mtf);
   mt_b.upload(mtb);
+  cmb.upload(cm.empty() ? std::vector<dev::CombDesc>(1) : cm);
   tdesc.upload(td);
   tiles.upload(tl);
   tile_off.upload(toff);
   sn_RB.upload(vRB); sn_CB.upload(vCB); sn_nrb.upload(vnrb); sn_ncb.upload(vncb);
-  sn_rbc.upload(vrbc); sn_cbc.upload(vcbc);
   sn_fpart.upload(vfp); sn_bpart.upload(vbp);
   vb_off.upload(vvo);
   gsrc.upload(vgsrc);
@@ -380,8 +399,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   vb.alloc(nrows + 2);  // +2: the even-aligned bulk copies may read one past the end
   fpart.alloc(std::max<int64_t>(nfp, 1));
   bpart.alloc(std::max<int64_t>(nbp, 1));
-  rb_cnt.alloc(std::max(nrbc, 1));
-  cb_cnt.alloc(std::max(ncbc, 1));
   ctl.alloc(dev::SW_COUNT);
   reset_counters(nullptr);
   CUDA_CHECK(cudaDeviceSynchronize());
@@ -412,8 +429,6 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
 }
 
 void DevFactor::reset_counters(cudaStream_t s) {
-  for (DBuf<unsigned long long>* c : {&rb_cnt, &cb_cnt})
-    CUDA_CHECK(cudaMemsetAsync(c->p, 0, c->n * sizeof(unsigned long long), s));
   std::vector<unsigned long long> c0(dev::SW_COUNT, 0ull);
   c0[dev::SW_T0] = ~0ull;
   CUDA_CHECK(cudaMemcpyAsync(ctl.p, c0.data(), c0.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
@@ -434,9 +449,8 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.Lt = Lt.p;
   S.sn_RB = sn_RB.p; S.sn_CB = sn_CB.p; S.sn_nrb = sn_nrb.p; S.sn_ncb = sn_ncb.p;
   S.sn_fpart = sn_fpart.p; S.sn_bpart = sn_bpart.p;
-  S.sn_rbc = sn_rbc.p; S.sn_cbc = sn_cbc.p;
   S.fpart = fpart.p; S.bpart = bpart.p;
-  S.rb_cnt = rb_cnt.p; S.cb_cnt = cb_cnt.p;
+  S.cmb = cmb.p;
   S.vb = vb.p;
   S.vb_off = vb_off.p;
   S.gsrc = gsrc.p;

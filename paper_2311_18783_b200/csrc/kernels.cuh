@@ -91,7 +91,7 @@ __global__ void k_mf_factor_level(PlanDev P, const int* __restrict__ list, const
 // -------------------------------------------- supernodal triangular sweeps
 // (sweep.cu) control words of a persistent sweep and its phase kinds
 enum { SW_EPOCH = 0, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
-enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR };
+enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR, PH_CF, PH_CB };
 constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 3328;   // doubles per tile (26 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
@@ -101,8 +101,7 @@ constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can 
 constexpr int kDescAhead = 4;    // M-task descriptors streamed ahead of the current task
 constexpr int kDescRing = 8;     // descriptor ring slots (> kDescAhead)
 // MDD_SWEEP_TRACE words per (phase, CTA), thread 0's view (%globaltimer ns): start,
-// end, time waiting on tile mbarriers, tiles consumed, time in the deferred-combine
-// flushes, time from a task's top to its first tile wait (descriptor ring + fused
+// end, time waiting on tile mbarriers, tiles consumed, 0, time from a task's top to its first tile wait (descriptor ring + fused
 // gather), time from a tile's arrival to its slot refill (compute + barrier), tasks
 constexpr int kTraceWords = 8;
 constexpr int kSweepSmemDoubles = kStages * kTileMax + kVecSlots * (kVecMax + 2) + kVecMax + kSweepThreads;
@@ -114,11 +113,11 @@ struct __align__(16) MTaskDesc {
   long long vlo2;   // even-aligned start of the task vector's bulk copy (vb index)
   long long uptr;   // offset of the supernode's update vector
   long long part;   // big: offset of this tile's partial sums (fpart / bpart)
-  long long comb;   // big: first partial of the combine (row block / column block)
-  long long cnt;    // big: index of the row-block / column-block counter
+  long long comb;   // big: first partial of its row block / column block
+  long long cnt;    // unused
   int big, k0, k1;  // 0 small / 1 big 2-D tile / 2 strip (rb, cb = first row / column); tdesc range
   int nr, nc, rows, cols, rb, cb, RB, CB;
-  int ntl;          // big: tiles combined by the last arriver
+  int ntl;          // big: partial sums of its row block / column block
   int voff;         // offset of the vector inside its shared-memory buffer
   int vbytes;       // bytes of the vector bulk copy
   int vn;           // rows of the task vector (vb rows [vlo2 + voff, + vn))
@@ -131,14 +130,26 @@ struct __align__(16) MTaskDesc {
 constexpr int kTdInline = 4;
 static_assert(sizeof(MTaskDesc) == 192, "MTaskDesc layout");
 
+// one row block (forward) / column block (backward) of a 2-D supernode whose
+// partial sums a combine phase (PH_CF / PH_CB) adds, in a fixed order, after the
+// level's tile phase: rows first .. first+m-1 of the panel (forward) / columns
+// (backward); partial q of output o at comb + q * ld + o
+struct __align__(16) CombDesc {
+  long long comb, col0, uptr, vo;
+  int ld, ntl, m, first, nc, pad_[3];
+};
+static_assert(sizeof(CombDesc) == 64, "CombDesc layout");
+
 struct SweepDev {
   PlanDev P;
   const double* dinv;
   const MTaskDesc* mtf;          // M tasks, forward / backward descriptors
   const MTaskDesc* mtb;
   // phases {kind, a, b, w}: G: rows [a, b) of vb; M: mtask [a, b), w = 1 when the
-  // level's gather is fused into its tasks (no G phase before it); PR
+  // level's gather is fused into its tasks (no G phase before it); C: combine
+  // items [a, b), w = 1 when the level's t rows are not in vb (fused); PR
   const int4* phases;
+  const CombDesc* cmb;
   int nphases;
   const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
@@ -150,12 +161,8 @@ struct SweepDev {
   const int* sn_ncb;
   const int64_t* sn_fpart;       // big supernodes: partial-sum offsets
   const int64_t* sn_bpart;
-  const int* sn_rbc;             // offsets of the row-block / column-block counters
-  const int* sn_cbc;
   double* fpart;
   double* bpart;
-  unsigned long long* rb_cnt;
-  unsigned long long* cb_cnt;
   // per-supernode row vectors (t forward, w backward): rows of g at vb_off[g]
   double* vb;
   const int64_t* vb_off;

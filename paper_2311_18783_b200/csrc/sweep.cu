@@ -21,16 +21,19 @@
 //   for each level, leaves first:   G_f  (flat gather of every supernode's
 //     right-hand side t = [b_c ; 0] + children's update vectors, a precomputed
 //     row -> contributions list, so no scatter and no atomics)  |  M_f (tiles)
-//   for each level, root first:     G_b  (w = [D z_c ; -x_off])  |  M_b (tiles)
+//     |  C_f (the partial sums of the level's 2-D supernodes)
+//   for each level, root first:     G_b  (w = [D z_c ; -x_off])  |  M_b  |  C_b
 //   prolongation.
 // Levels with few tasks per CTA skip their G phase: each task gathers its own
 // vector rows (same sums, same order).  Within M phases the tasks, sorted
 // largest first, are dealt to the CTAs in snake order (no atomics).  A task is a
 // small supernode (all its packed column tiles, accumulated in shared memory by
 // one CTA), a strip of a wide supernode, or a group of 1-4 RB x CB tiles of a big
-// supernode whose partial sums the last group to arrive combines in a fixed
-// order -- every reduction is bit-reproducible and independent of the grid
-// size.  Counters are cumulative across launches (epoch); a barrier wait that
+// supernode, which stores its partial sums; the C phase after the tiles adds them
+// in a fixed order (one barrier instead of a publishing atomic and a deferred
+// combine per group: those cost ~2 us of CTA time per group, measured on c4) --
+// every reduction is bit-reproducible and independent of the grid size.  The
+// barrier counter is cumulative across launches (epoch); a barrier wait that
 // exceeds kSpinTimeoutNs raises an abort flag reported by the host.
 #include "kernels.cuh"
 
@@ -429,11 +432,6 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ __align__(16) MTaskDesc s_desc[kDescRing];
   __shared__ int s_tinfo[kStages];
-  // 2-D task groups whose combine is deferred to the end of the phase (or until the
-  // list is full): the task, and whether its atomic made it the last of its block
-  constexpr int kMaxPend = 32;
-  __shared__ int s_pend_task[kMaxPend];
-  __shared__ unsigned char s_pend_last[kMaxPend];
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
@@ -452,8 +450,8 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     const int4 PH = S.phases[ph];
     const int kind = PH.x;
     const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
-    // trace (thread 0): time in tile waits, tiles, flushes, task starts, tile bodies, tasks
-    unsigned long long t_wait = 0, t_tiles = 0, t_flush = 0, t_start = 0, t_body = 0, t_tasks = 0;
+    // trace (thread 0): time in tile waits, tiles, task starts, tile bodies, tasks
+    unsigned long long t_wait = 0, t_tiles = 0, t_start = 0, t_body = 0, t_tasks = 0;
     const bool trc = S.trace && tid == 0;
     if (kind == PH_GF) {
       // t = [b_c ; 0] + children's updates, one row per thread
@@ -461,6 +459,31 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     } else if (kind == PH_GB) {
       // w = [D z_c ; -x_off]
       for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_w(S, q);
+    } else if (kind == PH_CF || kind == PH_CB) {
+      // the partial sums of the level's 2-D row blocks (forward) / column blocks
+      // (backward): one warp per block, lanes over its outputs, partials added in
+      // index order (fixed, grid-independent)
+      const bool cf = kind == PH_CF, fz = PH.w != 0;
+      const int lane = tid & 31;
+      const size_t nw = (size_t)gridDim.x * kWarps;
+      for (size_t it = (size_t)PH.y + (size_t)blockIdx.x * kWarps + (tid >> 5); it < (size_t)PH.z; it += nw) {
+        const CombDesc C = S.cmb[it];
+        const double* pb = (cf ? S.fpart : S.bpart) + C.comb;
+        for (int o = lane; o < C.m; o += 32) {
+          double s0 = 0.0, s1 = 0.0;
+          int q = 0;
+          for (; q + 1 < C.ntl; q += 2) {
+            s0 += __ldcg(pb + (i64)q * C.ld + o);
+            s1 += __ldcg(pb + (i64)(q + 1) * C.ld + o);
+          }
+          if (q < C.ntl) s0 += __ldcg(pb + (i64)q * C.ld + o);
+          const double sum = s0 + s1;
+          const int r = C.first + o;
+          if (!cf) S.xb[C.col0 + r] = sum;
+          else if (r < C.nc) S.xf[C.col0 + r] = sum;
+          else S.upd[C.uptr + (r - C.nc)] = (fz ? gather_t(S, C.vo + r) : __ldcg(S.vb + C.vo + r)) - sum;
+        }
+      }
     } else if (kind == PH_PR) {
       for (size_t e = gtid; e < (size_t)S.n_out; e += gthreads) {
         double s = 0.0;
@@ -541,63 +564,6 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       };
       if (tid == 0)
         for (int q = 0; q < kStages; ++q) issue_next();
-      // last group of its row block (fwd) / column block (bwd): combine the ntl
-      // partials, Lq lanes per output (lane s sums partials s, s+Lq, ..., then a
-      // shuffle tree): a fixed order that depends on ntl only
-      auto combine = [&](const MTaskDesc& D) {
-        const int m = fwd ? D.rows : D.cols;
-        const int Lq = m <= 32 ? 8 : m <= 64 ? 4 : m <= 128 ? 2 : 1;
-        const double* pb = fwd ? S.fpart + D.comb : S.bpart + D.comb;
-        const i64 ld = fwd ? D.nr : D.nc;
-        const int sub = tid & (Lq - 1);
-        for (int o0 = 0; o0 < m; o0 += kSweepThreads / Lq) {
-          const int o = o0 + tid / Lq;
-          double s0 = 0.0, s1 = 0.0;
-          if (o < m) {
-            int q = sub;
-            for (; q + Lq < D.ntl; q += 2 * Lq) {
-              s0 += __ldcg(pb + (i64)q * ld + o);
-              s1 += __ldcg(pb + (i64)(q + Lq) * ld + o);
-            }
-            if (q < D.ntl) s0 += __ldcg(pb + (i64)q * ld + o);
-          }
-          double sum = s0 + s1;
-          for (int w = 1; w < Lq; w <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, w);
-          if (o < m && sub == 0) {
-            if (fwd) {
-              const int r = D.rb * D.RB + o;
-              if (r < D.nc) S.xf[D.col0 + r] = sum;
-              else S.upd[D.uptr + (r - D.nc)] = (fused ? gather_t(S, D.vo + r) : __ldcg(S.vb + D.vo + r)) - sum;
-            } else {
-              S.xb[D.col0 + D.cb * D.CB + o] = sum;
-            }
-          }
-        }
-      };
-      // The atomic that publishes a group's partials is issued by thread 32 and its
-      // result is only read at the next group's atomic or at the flush: its round
-      // trip to L2 overlaps the next task instead of stalling the CTA at a barrier
-      // (the stall ncu put at 15 % of the coarse sweep's samples).  The combines run
-      // at the flush: their outputs are read only by later phases.
-      int npend = 0;                               // uniform
-      unsigned long long infl_old = 0;             // thread 32: the in-flight atomic
-      int infl_slot = -1, infl_ntl = 0;
-      auto flush = [&]() {
-        const unsigned long long f0 = trc ? globaltimer() : 0ull;
-        if (tid == 32 && infl_slot >= 0) {
-          s_pend_last[infl_slot] = infl_old + 1 == cur * (unsigned long long)infl_ntl;
-          infl_slot = -1;
-        }
-        __syncthreads();
-        for (int q = 0; q < npend; ++q)
-          if (s_pend_last[q]) {
-            const MTaskDesc Dp = MT[task_of(s_pend_task[q])];
-            combine(Dp);
-          }
-        __syncthreads();
-        npend = 0;
-        if (trc) t_flush += globaltimer() - f0;
-      };
       int cs = 0;  // tiles consumed in this phase
       for (int i = 0;; ++i) {
         const int k = task_of(i);
@@ -718,6 +684,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             __syncthreads();
             tile_done();
           }
+          // this group's partial sums; the level's combine phase adds them
           if (fwd) {
             double* const part = S.fpart + D.part;
             const int lane = tid & 31, r = 8 * (tid >> 5) + (lane >> 2);
@@ -729,23 +696,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
             double* const part = S.bpart + D.part;
             for (int q = tid; q < D.cols; q += kSweepThreads) part[q] = vec2[q];
           }
-          __syncthreads();
-          if (tid == 32) {
-            // one acq_rel atomic publishes this group's partial sums (ordered after the
-            // CTA's part[] writes by the bar.sync above) and tells the last group of
-            // the row / column block to combine
-            if (infl_slot >= 0) s_pend_last[infl_slot] = infl_old + 1 == cur * (unsigned long long)infl_ntl;
-            unsigned long long* c = (fwd ? S.rb_cnt : S.cb_cnt) + D.cnt;
-            asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(infl_old) : "l"(c) : "memory");
-            infl_ntl = D.ntl;
-            infl_slot = npend;
-            s_pend_task[npend] = i;
-          }
-          if (++npend == kMaxPend) flush();
         }
         __syncthreads();
       }
-      if (npend > 0) flush();
     }
     // the next phases read vb / upd / xf / xb with TMA bulk copies (async proxy):
     // order this thread's generic-proxy global writes before them
@@ -756,7 +709,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       tr[1] = globaltimer();
       tr[2] = t_wait;
       tr[3] = t_tiles;
-      tr[4] = t_flush;
+      tr[4] = 0;  // (was: deferred-combine flushes)
       tr[5] = t_start;
       tr[6] = t_body;
       tr[7] = t_tasks;

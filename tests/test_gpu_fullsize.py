@@ -189,18 +189,35 @@ def _geneo_golden(cfg):
 
 def test_geneo_counts_full_size_c1(c1):
     """GenEO counts of every subdomain of the full-size c1 bit-exact against the
-    oracle's per-subdomain dense GEVPs (tests/golden/geneo_c1_full.json), the kept
-    eigenvalues at 10x the difference observed on the c1 recipe at 8^3."""
-    from parity_observed import OBSERVED
+    oracle's per-subdomain dense GEVPs (tests/golden/geneo_c1_full.json).  The kept
+    eigenvalues: GEVP 3.5 (eq. 3.1) at contrast 1e4, gamma = 1e-4 moves
+    them by up to 2.2e-4 relative when the ORACLE itself only sums the element
+    matrices in another order (tests/golden/geneo_c1_full_order_sensitivity.json,
+    tools/geneo_order_sensitivity.py; the device's slot-ordered assembly is one more
+    such order).  Tolerance: 10x that measured sensitivity on the subdomains the
+    channels cross; 1e-9 on the subdomains whose eigenvalues did not move (< 1e-12)."""
+    import json
+    import os
     g = _geneo_golden("c1")
     if g is None or len(g["count"]) < g["nsub"]:
         pytest.skip("geneo_c1_full golden not generated")
+    sens = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                       "geneo_c1_full_order_sensitivity.json")))["max_rel"]
     w, G, A, dec = c1
-    cnt = G.int_array("geneo_count")
-    assert [int(c) for c in cnt] == [g["count"][str(i)] for i in range(g["nsub"])]
+    cnt = [int(c) for c in G.int_array("geneo_count")]
+    assert cnt == [g["count"][str(i)] for i in range(g["nsub"])]
     lam = G.double_array("geneo_lambda")
-    lo = np.concatenate([np.asarray(g["lambda"][str(i)]) for i in range(g["nsub"])])
-    assert np.max(np.abs(lam - lo) / lo) <= 10 * OBSERVED["c1-recipe-8"]["geneo_lambda_rel"]
+    smax = max(sens.values())
+    off = 0
+    for i in range(g["nsub"]):
+        lo = np.asarray(g["lambda"][str(i)])
+        li = lam[off:off + cnt[i]]
+        off += cnt[i]
+        if not len(lo):
+            continue
+        rel = float(np.max(np.abs(li - lo) / lo))
+        tol = 1e-9 if sens[str(i)] < 1e-12 else 10 * smax
+        assert rel <= tol, (i, rel, sens[str(i)])
 
 
 @pytest.fixture(scope="module")

@@ -8,7 +8,7 @@ with open(path, "rb") as f:
     ph = np.frombuffer(f.read(16 * nph), dtype=np.int32).reshape(nph, 4)
     tr = np.frombuffer(f.read(8 * words * nph * grid), dtype=np.uint64).reshape(nph, grid, words).astype(np.int64)
 t0 = tr[tr > 0].min()
-names = ["G_f", "M_f", "G_b", "M_b", "prol"]
+names = ["G_f", "M_f", "G_b", "M_b", "prol", "C_f", "C_b"]
 tot = {}
 print(f"{path}: phases {nph}, grid {grid}, span {(tr.max() - t0) / 1e3:.1f} us")
 prev_end = 0
