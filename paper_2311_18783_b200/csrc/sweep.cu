@@ -43,6 +43,7 @@ namespace dev {
 namespace {
 constexpr unsigned long long kSpinTimeoutNs = 4000000000ull;  // 4 s
 constexpr int kWarps = kSweepThreads / 32;
+constexpr int kGatherRows = 4;  // rows per thread in flight in the flat gather phases
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
@@ -454,34 +455,85 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
     unsigned long long t_wait = 0, t_tiles = 0, t_start = 0, t_body = 0, t_tasks = 0;
     const bool trc = S.trace && tid == 0;
     if (kind == PH_GF) {
-      // t = [b_c ; 0] + children's updates, one row per thread
-      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_t(S, q);
+      // t = [b_c ; 0] + children's updates: 4 rows per thread interleaved (their
+      // dependent loads in flight together), each row's sum in its fixed order
+      const size_t lo = PH.y, hi = PH.z;
+      for (size_t q0 = lo + gtid; q0 < hi; q0 += kGatherRows * gthreads) {
+        double v[kGatherRows];
+        i64 c0[kGatherRows], c1[kGatherRows];
+#pragma unroll
+        for (int k = 0; k < kGatherRows; ++k) {
+          const size_t q = q0 + k * gthreads;
+          int src = -1;
+          c0[k] = c1[k] = 0;
+          if (q < hi) { src = S.gsrc[q]; c0[k] = S.cptr[q]; c1[k] = S.cptr[q + 1]; }
+          v[k] = src >= 0 ? __ldg(S.b + src) : 0.0;
+        }
+        for (int j = 0;; ++j) {
+          bool any = false;
+#pragma unroll
+          for (int k = 0; k < kGatherRows; ++k)
+            if (c0[k] + j < c1[k]) { v[k] += __ldcg(S.upd + S.cidx[c0[k] + j]); any = true; }
+          if (!any) break;
+        }
+#pragma unroll
+        for (int k = 0; k < kGatherRows; ++k)
+          if (q0 + k * gthreads < hi) S.vb[q0 + k * gthreads] = v[k];
+      }
     } else if (kind == PH_GB) {
-      // w = [D z_c ; -x_off]
-      for (size_t q = (size_t)PH.y + gtid; q < (size_t)PH.z; q += gthreads) S.vb[q] = gather_w(S, q);
+      // w = [D z_c ; -x_off], 4 rows per thread interleaved
+      const size_t lo = PH.y, hi = PH.z;
+      for (size_t q0 = lo + gtid; q0 < hi; q0 += kGatherRows * gthreads) {
+        i64 w[kGatherRows];
+#pragma unroll
+        for (int k = 0; k < kGatherRows; ++k) w[k] = q0 + k * gthreads < hi ? S.wsrc[q0 + k * gthreads] : 0;
+        double v[kGatherRows], d[kGatherRows];
+#pragma unroll
+        for (int k = 0; k < kGatherRows; ++k) {
+          if (w[k] < 0) { v[k] = -__ldcg(S.xb + (-w[k] - 1)); d[k] = 0.0; }
+          else { v[k] = __ldcg(S.xf + w[k]); d[k] = __ldg(S.dinv + w[k]); }
+        }
+#pragma unroll
+        for (int k = 0; k < kGatherRows; ++k)
+          if (q0 + k * gthreads < hi) S.vb[q0 + k * gthreads] = w[k] < 0 ? v[k] : d[k] != 0.0 ? v[k] / d[k] : 0.0;
+      }
     } else if (kind == PH_CF || kind == PH_CB) {
       // the partial sums of the level's 2-D row blocks (forward) / column blocks
-      // (backward): one warp per block, lanes over its outputs, partials added in
-      // index order (fixed, grid-independent)
+      // (backward): one warp per block, each lane two outputs (o, o + 32) with four
+      // partial chains each (eight loads in flight); fixed order, grid-independent:
+      // sum = (a0 + a1) + (a2 + a3), a_k = the partials q = k mod 4 in index order
       const bool cf = kind == PH_CF, fz = PH.w != 0;
       const int lane = tid & 31;
       const size_t nw = (size_t)gridDim.x * kWarps;
       for (size_t it = (size_t)PH.y + (size_t)blockIdx.x * kWarps + (tid >> 5); it < (size_t)PH.z; it += nw) {
         const CombDesc C = S.cmb[it];
         const double* pb = (cf ? S.fpart : S.bpart) + C.comb;
-        for (int o = lane; o < C.m; o += 32) {
-          double s0 = 0.0, s1 = 0.0;
+        for (int o = lane; o < C.m; o += 64) {
+          const bool two = o + 32 < C.m;
+          double a[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
           int q = 0;
-          for (; q + 1 < C.ntl; q += 2) {
-            s0 += __ldcg(pb + (i64)q * C.ld + o);
-            s1 += __ldcg(pb + (i64)(q + 1) * C.ld + o);
+          for (; q + 4 <= C.ntl; q += 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              a[k] += __ldcg(pb + (i64)(q + k) * C.ld + o);
+              if (two) e[k] += __ldcg(pb + (i64)(q + k) * C.ld + o + 32);
+            }
           }
-          if (q < C.ntl) s0 += __ldcg(pb + (i64)q * C.ld + o);
-          const double sum = s0 + s1;
-          const int r = C.first + o;
-          if (!cf) S.xb[C.col0 + r] = sum;
-          else if (r < C.nc) S.xf[C.col0 + r] = sum;
-          else S.upd[C.uptr + (r - C.nc)] = (fz ? gather_t(S, C.vo + r) : __ldcg(S.vb + C.vo + r)) - sum;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (q + k < C.ntl) {
+              a[k] += __ldcg(pb + (i64)(q + k) * C.ld + o);
+              if (two) e[k] += __ldcg(pb + (i64)(q + k) * C.ld + o + 32);
+            }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const double sum = h ? (e[0] + e[1]) + (e[2] + e[3]) : (a[0] + a[1]) + (a[2] + a[3]);
+            const int r = C.first + o + 32 * h;
+            if (!cf) S.xb[C.col0 + r] = sum;
+            else if (r < C.nc) S.xf[C.col0 + r] = sum;
+            else S.upd[C.uptr + (r - C.nc)] = (fz ? gather_t(S, C.vo + r) : __ldcg(S.vb + C.vo + r)) - sum;
+          }
         }
       }
     } else if (kind == PH_PR) {
