@@ -32,6 +32,7 @@ struct NDWork {
   const Csr* pat;
   const int32_t* xyz2;
   const int32_t* box = nullptr;  // deferred unknowns' coupling boxes (SymSystem::box)
+  int search_min = 0;            // > 0: sets this large search their cut plane (below)
   std::vector<int32_t> side;   // per vertex: -1 not in current set, 0 left, 1 right, 2 sep
   std::vector<int32_t> order;  // output: new -> old
   int leaf;
@@ -70,6 +71,49 @@ void nd_rec(NDWork& w, std::vector<int32_t>& V, std::vector<int32_t>& T) {
     int med = cs[nv / 2];
     // prefer an even (node-plane) value: in-plane edges then form an exact separator
     int cand[3] = {med - (med & 1), med + (med & 1), med};
+    if (w.search_min > 0 && (i64)nv >= w.search_min && w.box) {
+      // the coarse system: the median plane of a box partition lies on subdomain
+      // boundaries, where every node has a copy per overlapping subdomain and every
+      // adjacent subdomain's GenEO columns cross the cut.  Take, among the node
+      // planes of the middle half, the one with the smallest separator + crossing
+      // deferred columns (the dense root and its ancestors grow with its square).
+      for (int32_t v : V) w.side[v] = 0;
+      std::vector<int32_t> maxc(nv);
+      for (size_t k = 0; k < nv; ++k) {
+        const int32_t v = V[k];
+        int32_t m2 = w.xyz2[3 * v + axis];
+        for (i64 p = w.pat->ptr[v]; p < w.pat->ptr[v + 1]; ++p) {
+          const int32_t u = w.pat->idx[p];
+          if (w.side[u] >= 0) m2 = std::max(m2, w.xyz2[3 * u + axis]);
+        }
+        maxc[k] = m2;
+      }
+      for (int32_t v : V) w.side[v] = -1;
+      std::vector<int32_t> sc(cs);
+      std::sort(sc.begin(), sc.end());
+      const int32_t qlo = sc[nv / 4], qhi = sc[(3 * nv) / 4];
+      i64 best = INT64_MAX;
+      int bs = cand[0];
+      for (int32_t sp = qlo + (qlo & 1); sp <= qhi; sp += 2) {
+        i64 nl = 0, nr = 0, ns = 0;
+        for (size_t k = 0; k < nv; ++k) {
+          const int32_t c = w.xyz2[3 * V[k] + axis];
+          if (c == sp) ++ns;
+          else if (c > sp) ++nr;
+          else if (maxc[k] > sp) ++ns;
+          else ++nl;
+        }
+        if (4 * nl < (i64)nv || 4 * nr < (i64)nv) continue;
+        i64 nts = 0;
+        for (int32_t t : T) {
+          const int32_t* b = w.box + 6 * t;
+          if (!(b[3 + axis] < sp) && !(b[axis] > sp)) ++nts;
+        }
+        const i64 score = ns + nts;
+        if (score < best || (score == best && std::abs(sp - med) < std::abs(bs - med))) { best = score; bs = sp; }
+      }
+      cand[0] = bs;
+    }
     for (int ci = 0; ci < 3 && !done; ++ci) {
       int s = cand[ci];
       L.clear(); R.clear(); S.clear();
@@ -161,6 +205,7 @@ void analyse_one(Sys1& s, const SymSystem& sys, int leaf) {
   s.n = n;
   NDWork w;
   w.pat = &A; w.xyz2 = sys.xyz2; w.leaf = leaf; w.box = sys.box;
+  w.search_min = getenv("MDD_ND_SEARCH") ? atoi(getenv("MDD_ND_SEARCH")) : 20000;
   w.side.assign(n, -1);
   std::vector<int32_t> V, tail, none;
   for (int v = 0; v < n; ++v) (sys.last && sys.last[v] ? tail : V).push_back(v);
