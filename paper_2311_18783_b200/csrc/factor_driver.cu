@@ -63,7 +63,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   // copies of the panel; no partial sums).  2-D (nr > kVecMax): RB x CB tiles
   // whose partial sums the last tile of a row / column block combines.
   // tiles[] = {g, a, b, kind}: kind 0 = 2-D (a = rb, b = cb), 1 = forward strip
-  // (a = first row), 2 = backward strip (b = first column), 3 = small column tile
+  // (a = first row, b = rows), 2 = backward strip (a = columns, b = first column),
+  // 3 = small column tile
   const int nsn = fp.nsn;
   std::vector<int> vRB(nsn), vCB(nsn), vnrb(nsn, 1), vncb(nsn, 1);
   std::vector<uint8_t> mode(nsn);  // 0 small, 1 strip, 2 2-D
@@ -101,10 +102,23 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       }
       bt[g] = ft[g];
     } else if (mode[g] == 1) {
-      const int rs = std::max(1, dev::kTileMax / nc), cs = std::max(1, dev::kTileMax / nr);
-      vRB[g] = rs; vCB[g] = cs;
-      for (int r0 = 0; r0 < nr; r0 += rs) ft[g].push_back(add_tile(make_int4(g, r0, 0, 1), std::min(rs, nr - r0), nc));
-      for (int c0 = 0; c0 < nc; c0 += cs) bt[g].push_back(add_tile(make_int4(g, 0, c0, 2), nr, std::min(cs, nc - c0)));
+      // strips store only the lower trapezoid they touch: forward row strip
+      // [r0, r0+rows) x columns [0, min(nc, r0+rows)), backward column strip
+      // [c0, c0+cols) x rows [c0, nr) (the panel is zero above its diagonal); as
+      // many rows / columns per tile as fit kTileMax
+      vRB[g] = nr; vCB[g] = nc;
+      for (int r0 = 0; r0 < nr;) {
+        int rows = 1;
+        while (r0 + rows < nr && (int64_t)(rows + 1) * std::min(nc, r0 + rows + 1) <= dev::kTileMax) ++rows;
+        ft[g].push_back(add_tile(make_int4(g, r0, rows, 1), rows, std::min(nc, r0 + rows)));
+        r0 += rows;
+      }
+      for (int c0 = 0; c0 < nc;) {
+        int cols = 1;
+        while (c0 + cols < nc && (int64_t)(cols + 1) * (nr - c0) <= dev::kTileMax) ++cols;
+        bt[g].push_back(add_tile(make_int4(g, cols, c0, 2), nr - c0, cols));
+        c0 += cols;
+      }
     } else {
       // a task's vector (up to kGroup row blocks / column blocks) must fit a
       // kVecMax shared-memory slot: RB, CB <= kVecMax / kGroup
@@ -243,9 +257,9 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
           for (int t : tiles_g) {
             dev::MTaskDesc X = D;
             X.big = 2;
-            X.rows = rc[t].x; X.cols = rc[t].y;
-            X.rb = tl[t].y;
-            X.cb = tl[t].z;
+            X.rows = rc[t].x; X.cols = rc[t].y;  // fwd: rows x columns [0, cols); bwd: nr - cb rows
+            X.rb = dir == 0 ? tl[t].y : tl[t].z;  // first row
+            X.cb = dir == 0 ? 0 : tl[t].z;        // first column
             set_vec(X, vvo[g], vvo[g] + nr);
             lt.push_back({tile_bytes(t), X, {t}});
           }

@@ -672,20 +672,21 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
 #endif
         if (D.big == 2) {
           // ---------------- strip of a wide supernode (nr <= kVecMax): fwd = rows
-          // [r0, r0+rows) x all columns, bwd = all rows x columns [c0, c0+cols);
-          // the task vector is the whole t (fwd) / w (bwd): no partial sums
+          // [r0, r0+rows) x columns [0, cols), bwd = rows [c0, nr) x columns
+          // [c0, c0+cols) (the lower trapezoid it touches); the task vector is the
+          // whole t (fwd) / w (bwd): no partial sums
           next_tile_and_wait(D.k0);
           const double* T = sm + buf * kTileMax;
           if (fwd) {
             double* const upd = S.upd + D.uptr;
-            tile_matvec(T, D.rows, D.nc, vv, red, [&](int i2, double y) {
+            tile_matvec(T, D.rows, D.cols, vv, red, [&](int i2, double y) {
               const int r = D.rb + i2;
               if (r < D.nc) S.xf[D.col0 + r] = y;
               else upd[r - D.nc] = vv[r] - y;
             });
           } else {
             double* const xb = S.xb + D.col0 + D.cb;
-            tile_matvec_t(T, D.nr, D.cols, vv, red, [&](int j, double y) { xb[j] = y; });
+            tile_matvec_t(T, D.nr - D.cb, D.cols, vv + D.cb, red, [&](int j, double y) { xb[j] = y; });
           }
           __syncthreads();
           tile_done();
@@ -780,8 +781,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
 }
 
 // relayout of the column-major panels into contiguous tiles (setup).  tiles[k] =
-// {g, a, b, kind}: 0 2-D (rb, cb), 1 forward row strip (first row a, all columns),
-// 2 backward column strip (all rows, first column b), 3 small packed column tile
+// {g, a, b, kind}: 0 2-D (rb, cb), 1 forward row strip (first row a, b rows,
+// columns [0, min(nc, a + b))), 2 backward column strip (a columns from b, rows
+// [b, nr)), 3 small packed column tile
 // (a = columns, b = first column)
 __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict__ L,
                                 const int64_t* __restrict__ lptr) {
@@ -796,9 +798,9 @@ __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict
     r0 = tl.y * RB; c0 = tl.z * CB;
     rows = min(RB, nr - r0); cols = min(CB, nc - c0);
   } else if (kind == 1) {
-    r0 = tl.y; rows = min(RB, nr - r0);
+    r0 = tl.y; rows = tl.z; cols = min(nc, r0 + rows);
   } else {
-    c0 = tl.z; cols = min(CB, nc - c0);
+    c0 = tl.z; cols = tl.y; r0 = c0; rows = nr - c0;
   }
   double* dst = const_cast<double*>(S.Lt) + S.tile_off[k];
   if (kind == 3) {
