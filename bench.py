@@ -324,7 +324,7 @@ def main():
         G.set_variant(args.variant)
 
     info = G._info()   # after the solves: kernels per iteration, launches
-    roof = roofline(G, sweep_ms, in_step, csweep_ms, cin_step, t_ms)
+    roof = roofline(G, sweep_ms, in_step, csweep_ms, cin_step, t_ms, cfg=args.config)
     # the whole PCG iteration against the same roofline: algorithmic bytes of one
     # iteration (MaxwellDD.bytes_model) x iterations / device time
     bm = G.bytes_model()
@@ -368,7 +368,7 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=None):
+def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=None, cfg=None):
     """Dominant kernel of the step against the measured HBM copy bandwidth
     (MEASURED_PEAKS.json): of the two persistent supernodal sweeps (k_sweep) -- the
     local solves M_AS and the coarse solve E^{-1}, one launch each per PCG
@@ -393,10 +393,14 @@ def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=N
                   "achieved": cb / (csweep_ms / 1e3) / 1e9, "avg_launch_ms_in_step": cin_step[0],
                   "achieved_in_step": c_in, "launches_in_step": cin_step[1]}
     achieved_in_step = b / (in_step[0] / 1e3) / 1e9 if in_step[0] > 0 else None
-    traffic = None
-    try:  # DRAM bytes of one k_sweep (local) launch from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "ncu_sweep_local.json")) as fh:
-            traffic = float(json.load(fh)["dram_bytes_per_launch"])
+    traffic = {}
+    try:  # DRAM bytes per launch of both sweeps from the committed ncu --set full capture
+        # (tools/gpu_profile_round.sh: tools/ncu_c4.py sweeps launches the local sweep, then E^-1)
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_sweeps_c4.json")) as fh:
+            cap = json.load(fh)
+        if cfg == "c4" and len(cap) == 2:
+            traffic = {"local": float(cap[0]["dram_bytes_per_launch"]),
+                       "coarse": float(cap[1]["dram_bytes_per_launch"])}
     except Exception:
         pass
     local = {"kernel": "k_sweep (local solves: gather, L y = b, D^-1, L^T x = z, prolong)",
@@ -413,10 +417,15 @@ def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=N
             k["frac_in_step"] = k["achieved_in_step"] / peak if k["achieved_in_step"] else None
             if total_ms:   # in-kernel time of all its launches / the timed region's device time
                 k["share_of_step"] = k["avg_launch_ms_in_step"] * k["launches_in_step"] / total_ms
-    if traffic is not None and main is not local:
-        traffic = None  # the committed ncu capture is of the local sweep
+    if local is not None:
+        local["traffic"] = traffic.get("local")
+    if coarse is not None:
+        coarse["traffic"] = traffic.get("coarse")
     out = {"bound": "hbm", "kernel": main["kernel"], "achieved": main["achieved"], "peak": peak, "unit": "GB/s",
-           "frac": main["achieved"] / peak, "traffic": traffic, "peak_source": src,
+           "frac": main["achieved"] / peak, "traffic": main.get("traffic"),
+           "traffic_source": "profiles/r02_ncu_sweeps_c4.json (dram__bytes_read.sum + dram__bytes_write.sum, "
+                             "one ncu --set full launch)" if main.get("traffic") else None,
+           "peak_source": src,
            "bytes_per_launch": main["bytes_per_launch"], "avg_launch_ms": main["avg_launch_ms"],
            "avg_launch_ms_in_step": main["avg_launch_ms_in_step"], "achieved_in_step": main["achieved_in_step"],
            "frac_in_step": main["frac_in_step"], "launches_in_step": main["launches_in_step"],
