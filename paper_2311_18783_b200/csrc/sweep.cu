@@ -40,6 +40,10 @@
 namespace mdd {
 namespace dev {
 
+#ifdef MDD_DEBUG_NOCOMPUTE
+// experiment builds only (tools/time_sweeps.py --nocompute): set after the setup
+__device__ int g_nocompute = 0;
+#endif
 namespace {
 constexpr unsigned long long kSpinTimeoutNs = 4000000000ull;  // 4 s
 constexpr int kWarps = kSweepThreads / 32;
@@ -662,7 +666,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
           ++cs;
         };
 #ifdef MDD_DEBUG_NOCOMPUTE
-        if (true) {  // timing experiment: stream the tiles, skip the arithmetic
+        if (g_nocompute) {  // timing experiment: stream the tiles, skip the arithmetic
           for (int kk = D.k0; kk < D.k1; ++kk) {
             next_tile_and_wait(kk);
             __syncthreads();
@@ -828,3 +832,9 @@ __global__ void k_tile_relayout(SweepDev S, int ntiles, const double* __restrict
 
 }  // namespace dev
 }  // namespace mdd
+
+#ifdef MDD_DEBUG_NOCOMPUTE
+extern "C" int mdd_debug_set_nocompute(int on) {
+  return (int)cudaMemcpyToSymbol(mdd::dev::g_nocompute, &on, sizeof(int));
+}
+#endif

@@ -22,7 +22,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
 __global__ void ring(const double* __restrict__ src, size_t nwords, int tile_bytes, int stages, int tiles,
                      double* out) {
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t mbar[16];
+  __shared__ __align__(8) uint64_t mbar[16];  // stages <= 16
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int q = 0; q < stages; ++q) mbar_init(&mbar[q]);

@@ -18,6 +18,9 @@ f = torch.as_tensor(workloads.rhs(n, w.f_seed), device="cuda")
 x = torch.empty_like(f)
 G.solve(f, x, tol=1e-8, maxit=1)      # graph built, everything warm
 torch.cuda.synchronize()
+if os.environ.get("MDD_NOCOMPUTE"):   # experiment build only (-DMDD_DEBUG_NOCOMPUTE): tiles streamed, no math
+    from paper_2311_18783_b200 import _lib
+    assert _lib.lib().mdd_debug_set_nocompute(1) == 0
 torch.cuda.profiler.start()            # ncu --profile-from-start off: only the hot path below
 if mode == "solve":
     # eager path (the graph's conditional WHILE node cannot be profiled by ncu):

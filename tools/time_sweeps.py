@@ -35,10 +35,19 @@ def timed(fn, reps=10):
     return e0.elapsed_time(e1) / reps
 
 
+if "--nocompute" in sys.argv:   # experiment build (MDD_NVCC_FLAGS=-DMDD_DEBUG_NOCOMPUTE): tiles streamed, no math
+    from paper_2311_18783_b200 import _lib
+    print(json.dumps({"with_math_local_ms": timed(lambda: G.apply_local(v, y)),
+                      "with_math_coarse_ms": timed(lambda: G.apply_coarse_inverse(v0, y0))}))
+    assert _lib.lib().mdd_debug_set_nocompute(1) == 0
 bm = G.bytes_model()
 tl = timed(lambda: G.apply_local(v, y))
 tc = timed(lambda: G.apply_coarse_inverse(v0, y0))
 cb = 16 * G.info["coarse_factor_nnz"] + 16 * n0
+if "--sweeps-only" in sys.argv:
+    print(json.dumps({"cfg": cfg, "local_ms": tl, "local_GBs": bm["local"] / tl / 1e6, "coarse_ms": tc,
+                      "coarse_GBs": cb / tc / 1e6}))
+    sys.exit(0)
 f = torch.as_tensor(workloads.rhs(n, w.f_seed), device="cuda")
 x = torch.empty_like(f)
 G.solve(f, x, tol=1e-8)
