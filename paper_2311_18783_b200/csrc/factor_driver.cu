@@ -520,7 +520,21 @@ void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* s
   S.b = b;
   S.out = out;
   S.stop = stop;
-  dev::k_sweep<<<sweep_grid, dev::kSweepThreads, dev::kSweepSmemDoubles * sizeof(double), s>>>(S);
+  // a cooperative launch: the persistent CTAs spin on grid barriers, so they must
+  // all be co-resident -- guaranteed by the launch (or it fails), not assumed from
+  // the occupancy calculator (other streams' kernels, MPS); the grid-barrier
+  // timeout stays as a backstop.  Captured into the solve graph like any launch.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sweep_grid);
+  cfg.blockDim = dim3(dev::kSweepThreads);
+  cfg.dynamicSmemBytes = dev::kSweepSmemDoubles * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, dev::k_sweep, S));
 }
 
 void DevFactor::check_abort(cudaStream_t s) {
