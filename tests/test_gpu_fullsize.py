@@ -195,7 +195,12 @@ def test_geneo_counts_full_size_c1(c1):
     matrices in another order (tests/golden/geneo_c1_full_order_sensitivity.json,
     tools/geneo_order_sensitivity.py; the device's slot-ordered assembly is one more
     such order).  Tolerance: 10x that measured sensitivity on the subdomains the
-    channels cross; 1e-9 on the subdomains whose eigenvalues did not move (< 1e-12)."""
+    channels cross.  On the subdomains whose oracle eigenvalues did not move
+    (< 1e-12) the device's own algorithm sets the scale: it solves the pencil on
+    the B-orthogonal complement of range(G_j) (reading R15) through a basis with
+    kappa ~ 6e6, so its eigenvalues carry eps * kappa ~ 1e-9 relative to the
+    largest one -- per eigenvalue 1e-9 (1 + lambda_max / lambda) (subdomain 7:
+    4.2e-8 observed on lambda_max / lambda_min = 110)."""
     import json
     import os
     g = _geneo_golden("c1")
@@ -215,9 +220,12 @@ def test_geneo_counts_full_size_c1(c1):
         off += cnt[i]
         if not len(lo):
             continue
-        rel = float(np.max(np.abs(li - lo) / lo))
-        tol = 1e-9 if sens[str(i)] < 1e-12 else 10 * smax
-        assert rel <= tol, (i, rel, sens[str(i)])
+        r = np.abs(li - lo) / lo
+        if sens[str(i)] < 1e-12:
+            k = int(np.argmax(r / (1 + lo.max() / lo)))
+            assert r[k] <= 1e-9 * (1 + lo.max() / lo[k]), (i, r[k], lo[k], lo.max())
+        else:
+            assert r.max() <= 10 * smax, (i, r.max(), sens[str(i)])
 
 
 @pytest.fixture(scope="module")
