@@ -225,6 +225,15 @@ enum {
 int mdd_shard_int_array(const mdd_setup_desc* desc, int rank, int nranks, int which, int64_t* out,
                         int64_t cap, int64_t* len);
 
+/* Host-only subtree-to-rank mapping of a supernode (elimination) tree, the one
+ * the sharded coarse solve applies to E's factor: nsn supernodes,
+ * parent[g] (< 0: a root), cost[g] (factor entries of supernode g); on return
+ * owner[g] = -1 for the replicated top supernodes (swept by every rank), else
+ * the rank in [0, nranks) that sweeps g together with its whole subtree.  All
+ * arrays HOST, caller-owned, nsn entries.  MDD_ERR_ARG on null arrays, bad
+ * parents or nranks < 1; nranks > 1 needs at least nranks leaf subtrees. */
+int mdd_tree_split(int nsn, const int32_t* parent, const int64_t* cost, int nranks, int32_t* owner);
+
 /* Sharded solve.  After mdd_setup of the whole problem on every
  * rank (the setup is replicated), mdd_shard_setup(h, rank, nranks) builds this
  * rank's hot-path data: its owned rows of A, the supernodal factor of its
@@ -232,10 +241,16 @@ int mdd_shard_int_array(const mdd_setup_desc* desc, int rank, int nranks, int wh
  * the halo exchange lists of mdd_shard_int_array.  The PCG vectors of a rank
  * are its owned dofs (MDD_SHARD_OWNED order, n_own of mdd_shard_info).  Only
  * MDD_VARIANT_AS2_COARSE_START (the coarse correction z = w + Q(r - A w) with
- * one n0-allreduce per iteration; E^{-1} is applied by every rank) and
- * MDD_VARIANT_AS1 are sharded.
+ * one n0-allreduce per iteration) and MDD_VARIANT_AS1 are sharded.  With
+ * nranks > 1, E^{-1} is applied distributed: the rank sweeps the subtrees of E's
+ * supernode tree that mdd_tree_split gives it plus the replicated top, with an
+ * allreduce of the frontier roots' update vectors between the two forward
+ * segments and an n0-allreduce of the solution (env
+ * MDD_SHARD_COARSE_REPLICATED=1: every rank sweeps the whole factor).
  * mdd_shard_info: out[0] n_own, [1] n_own + halo, [2] subdomains, [3] their
- *   factor entries.
+ *   factor entries, [4] 1 if the coarse solve is distributed, [5] coarse factor
+ *   entries this rank sweeps, [6] of which replicated top, [7] update entries
+ *   exchanged between the forward segments.
  * mdd_shard_nccl_init: NCCL communicator of the ranks (unique_id: the 128-byte
  *   ncclUniqueId of rank 0, broadcast by the caller, e.g. torch.distributed).
  * mdd_shard_solve: one rank's part of the sharded PCG; f_own / x_own: n_own

@@ -50,7 +50,8 @@ EXPORTS = ["mdd_setup", "mdd_destroy", "mdd_solve", "mdd_solve_host", "mdd_set_s
            "mdd_apply_operator", "mdd_apply_local", "mdd_apply_coarse", "mdd_apply_local_parts",
            "mdd_apply_coarse_inverse", "mdd_shard_setup", "mdd_shard_info", "mdd_shard_nccl_init",
            "mdd_shard_solve", "mdd_shard_solve_group", "mdd_info",
-           "mdd_get_int_array", "mdd_topology_int_array", "mdd_shard_int_array", "mdd_get_double_array",
+           "mdd_get_int_array", "mdd_topology_int_array", "mdd_shard_int_array", "mdd_tree_split",
+           "mdd_get_double_array",
            "mdd_phase_name", "mdd_set_profiling", "mdd_sweep_timing", "mdd_profile", "mdd_last_error"]
 
 
@@ -85,6 +86,7 @@ def load() -> C.CDLL:
         "mdd_get_int_array": (C.c_int, [P, C.c_int, lp, C.c_int64, lp]),
         "mdd_topology_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, lp, C.c_int64, lp]),
         "mdd_shard_int_array": (C.c_int, [C.POINTER(SetupDesc), C.c_int, C.c_int, C.c_int, lp, C.c_int64, lp]),
+        "mdd_tree_split": (C.c_int, [C.c_int, C.POINTER(C.c_int32), lp, C.c_int, C.POINTER(C.c_int32)]),
         "mdd_get_double_array": (C.c_int, [P, C.c_int, dp, C.c_int64, lp]),
         "mdd_phase_name": (C.c_char_p, [C.c_int]),
         "mdd_set_profiling": (C.c_int, [P, C.c_int]),

@@ -1043,6 +1043,15 @@ int mdd_shard_int_array(const mdd_setup_desc* d, int rank, int nranks, int which
   });
 }
 
+int mdd_tree_split(int nsn, const int32_t* parent, const int64_t* cost, int nranks, int32_t* owner) {
+  if (nsn < 0 || (nsn > 0 && (!parent || !cost || !owner))) { g_err = "null argument"; return MDD_ERR_ARG; }
+  return guard([&] {
+    std::vector<int32_t> o;
+    split_tree(nsn, parent, cost, nranks, o);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
 int mdd_get_int_array(mdd_handle h, int which, int64_t* out, int64_t cap, int64_t* len) {
   if (!h || !len) { g_err = "null argument"; return MDD_ERR_ARG; }
   return guard([&] {

@@ -92,6 +92,13 @@ struct DevFactor {
   const int64_t* pro_ptr = nullptr;
   const int32_t* pro_pos = nullptr;
   std::string name;
+  // a rank's view of a replicated factor (sharded coarse solve, sharded.cu):
+  // `base` holds the tiles and D^{-1}; role[g] = 1 the rank's subtrees (segment A),
+  // 2 the replicated top (segment B), 0 not swept.  Empty role: the whole factor.
+  const DevFactor* base = nullptr;
+  std::vector<int8_t> role;
+  int nph_a = 0;               // segment A = phases [0, nph_a), segment B = [nph_a, nphases)
+  int64_t swept_entries = 0;   // factor entries this schedule sweeps
   DevFactor() = default;
   DevFactor(const DevFactor&) = delete;
   ~DevFactor();
@@ -107,7 +114,8 @@ struct DevFactor {
   int factor(const double* src, int mode, double tol, uint8_t* dropped, cudaStream_t s);
   // x = A^{-1} b in one persistent launch; with `out` the result is prolongated
   // (out[e] = sum of its copies; needs upload(prolong_n > 0)), else it stays in xb.
-  void sweep(const double* b, double* out, cudaStream_t s, const int* stop = nullptr) const;
+  // seg: -1 every phase, 0 / 1 segment A / B of a view (empty segments launch nothing)
+  void sweep(const double* b, double* out, cudaStream_t s, const int* stop = nullptr, int seg = -1) const;
   // accumulated device time (ns) and count of sweep launches (SW_TSUM / SW_TCNT)
   void sweep_timing(unsigned long long* ns, unsigned long long* cnt, cudaStream_t s) const;
   // throws if a sweep aborted (barrier timeout); resets the schedule state

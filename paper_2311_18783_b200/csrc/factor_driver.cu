@@ -35,6 +35,8 @@ dev::PlanDev DevFactor::plan() const {
 
 void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t* pro_pos_dev,
                        const std::vector<int32_t>* gmap_host) {
+  MDD_REQUIRE(role.empty() || (int)role.size() == fp.nsn, 5, "sweep roles: one per supernode");
+  if (!base) {
   col0.upload(fp.sn_col0);
   ncol.upload(fp.sn_ncol);
   noff.upload(fp.sn_noff);
@@ -54,6 +56,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   parent.upload(fp.sn_parent);
   L.alloc(fp.lsize);
   dinv.alloc(fp.ntot);
+  }  // a view sweeps its base's factor (tiles, D^{-1}): no plan arrays, no panels
   upd.alloc(std::max<int64_t>(fp.usize, 1));
   xf.alloc(std::max<int64_t>(fp.ntot, 1));
   xb.alloc(std::max<int64_t>(fp.ntot, 1));
@@ -146,23 +149,41 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   auto tile_bytes = [&](int t) {
     return (int)((((int64_t)rc[t].x * rc[t].y + 1) & ~1LL) * (int64_t)sizeof(double));
   };
+  // ---- plan levels: the supernodes each level's phases sweep, in forward order.
+  // Whole factor: the factor's levels.  With roles (a rank of the sharded coarse
+  // solve): the levels of the rank's subtrees (role 1, segment A), then the levels
+  // of the replicated top (role 2, segment B); role 0 is not swept.
+  std::vector<std::vector<int>> plev;
+  int nlev_a = 0;
+  for (int seg = 0; seg < (role.empty() ? 1 : 2); ++seg) {
+    for (int l = 0; l < fp.nlevels; ++l) {
+      std::vector<int> v;
+      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
+        const int g = fp.level_sn[k];
+        if (role.empty() || role[g] == seg + 1) v.push_back(g);
+      }
+      if (!v.empty() || role.empty()) plev.push_back(std::move(v));
+    }
+    if (!role.empty() && seg == 0) nlev_a = (int)plev.size();
+  }
+  const int NL = (int)plev.size();
   // ---- per-level row vectors: rows of g at vb_off[g], each level contiguous
-  std::vector<int64_t> vvo(nsn), lev_row(fp.nlevels + 1, 0);
+  std::vector<int64_t> vvo(nsn, 0), lev_row(NL + 1, 0);
   int64_t nrows = 0;
-  for (int l = 0; l < fp.nlevels; ++l) {
+  for (int l = 0; l < NL; ++l) {
     lev_row[l] = nrows;
-    for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-      const int g = fp.level_sn[k];
+    for (const int g : plev[l]) {
       vvo[g] = nrows;
       nrows += fp.sn_ncol[g] + fp.sn_noff[g];
     }
   }
-  lev_row[fp.nlevels] = nrows;
+  lev_row[NL] = nrows;
   // forward gather: row -> b index (column rows) and children's update entries
   std::vector<int32_t> vgsrc(nrows, -1);
   std::vector<int64_t> vwsrc(nrows);
   std::vector<std::vector<int64_t>> contrib(nrows);
   for (int g = 0; g < nsn; ++g) {
+    if (!role.empty() && !role[g]) continue;
     const int nc = fp.sn_ncol[g], no = fp.sn_noff[g];
     const int64_t c0 = fp.sn_col0[g];
     for (int r = 0; r < nc; ++r) {
@@ -185,10 +206,10 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   // ---- M tasks per level and direction (largest first), packed descriptors
   std::vector<dev::MTaskDesc> mtf, mtb;
   std::vector<int4> td;
-  std::vector<int> lev_f(fp.nlevels + 1, 0), lev_b(fp.nlevels + 1, 0);
+  std::vector<int> lev_f(NL + 1, 0), lev_b(NL + 1, 0);
   // combine items (one per row block / column block of a 2-D supernode) per level
   std::vector<dev::CombDesc> cm;
-  std::vector<int> cmf(fp.nlevels + 1, 0), cmb_lev(fp.nlevels + 1, 0);
+  std::vector<int> cmf(NL + 1, 0), cmb_lev(NL + 1, 0);
   auto push_td = [&](int t) {
     // .x: tile id, or for packed small tiles first column | columns << 16 (the kernel
     // needs them per tile)
@@ -230,13 +251,12 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   for (int dir = 0; dir < 2; ++dir) {
     std::vector<dev::MTaskDesc>& out = dir == 0 ? mtf : mtb;
     std::vector<int>& lev = dir == 0 ? lev_f : lev_b;
-    for (int l = 0; l < fp.nlevels; ++l) {
+    for (int l = 0; l < NL; ++l) {
       lev[l] = (int)out.size();
      // the level's tasks with 2-D groups of kGroup tiles
      auto build_level = [&](const int kGroup) {
       std::vector<Cand> lt;
-      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-        const int g = fp.level_sn[k];
+      for (const int g : plev[l]) {
         const int nc = fp.sn_ncol[g], nr = nc + fp.sn_noff[g];
         dev::MTaskDesc D{};
         D.col0 = fp.sn_col0[g];
@@ -364,8 +384,8 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
         out.push_back(X);
       }
     }
-    lev[fp.nlevels] = (int)out.size();
-    if (dir == 0) cmf[fp.nlevels] = (int)cm.size(); else cmb_lev[fp.nlevels] = (int)cm.size();
+    lev[NL] = (int)out.size();
+    if (dir == 0) cmf[NL] = (int)cm.size(); else cmb_lev[NL] = (int)cm.size();
   }
   // levels with few tasks per CTA gather their task vectors inside the tasks (no
   // flat G phase and no grid barrier before them); the leaf levels keep the
@@ -375,14 +395,17 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     return lev[l + 1] - lev[l] <= fuse_tasks * plan_grid;
   };
   std::vector<int4> ph;
-  for (int l = 0; l < fp.nlevels; ++l) {
+  nph_a = 0;
+  for (int l = 0; l < NL; ++l) {
+    if (l == nlev_a && nlev_a > 0) nph_a = (int)ph.size();  // segment A ends: the rank's subtrees swept forward
     const bool fz = fused(lev_f, l);
     if (!fz) ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], fz ? 1 : 0));
     // the level's 2-D partial sums, added before any later phase reads xf / upd
     if (cmf[l + 1] > cmf[l]) ph.push_back(make_int4(dev::PH_CF, cmf[l], cmf[l + 1], fz ? 1 : 0));
   }
-  for (int l = fp.nlevels - 1; l >= 0; --l) {
+  if (nlev_a == NL && nlev_a > 0) nph_a = (int)ph.size();
+  for (int l = NL - 1; l >= 0; --l) {
     const bool fz = fused(lev_b, l);
     if (!fz) ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], fz ? 1 : 0));
@@ -420,6 +443,13 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     trace.alloc((size_t)dev::kTraceWords * nphases * sweep_grid);
     CUDA_CHECK(cudaMemset(trace.p, 0, trace.n * sizeof(unsigned long long)));
   }
+  if (base) MDD_REQUIRE(lt_size == base->lt_size && ntiles == base->ntiles, 5, "sweep view: tile layout differs from its base");
+  swept_entries = 0;
+  for (int g = 0; g < nsn; ++g)
+    if (role.empty() || role[g]) {
+      const int64_t nc = fp.sn_ncol[g], no = fp.sn_noff[g];
+      swept_entries += nc * (nc + 1) / 2 + nc * no;
+    }
   if (getenv("MDD_PLAN_STATS")) {
     int nbig = 0;
     for (int g = 0; g < nsn; ++g) nbig += mode[g] != 0;
@@ -427,16 +457,15 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
             "rows %lld contrib %lld grid %d\n", name.c_str(), nsn, nbig, fp.nlevels, (long long)fp.factor_nnz(),
             ntiles, 100.0 * (double)lt_size / std::max<double>(1.0, (double)fp.factor_nnz()), (int)mtf.size(),
             (long long)nrows, (long long)vcidx.size(), sweep_grid);
-    for (int l = 0; l < fp.nlevels; ++l) {
+    for (int l = 0; l < NL; ++l) {
       long long ent = 0;
       int big = 0;
-      for (int k = fp.level_ptr[l]; k < fp.level_ptr[l + 1]; ++k) {
-        const int g = fp.level_sn[k];
+      for (const int g : plev[l]) {
         ent += (long long)fp.sn_ncol[g] * (fp.sn_ncol[g] + fp.sn_noff[g]);
         big += mode[g] != 0;
       }
       fprintf(stderr, "  level %2d: sn %6d (big %4d) stored %10lld rows %8lld mtasks %6d\n", l,
-              fp.level_ptr[l + 1] - fp.level_ptr[l], big, ent, (long long)(lev_row[l + 1] - lev_row[l]),
+              (int)plev[l].size(), big, ent, (long long)(lev_row[l + 1] - lev_row[l]),
               lev_f[l + 1] - lev_f[l]);
     }
   }
@@ -452,15 +481,17 @@ void DevFactor::reset_counters(cudaStream_t s) {
 dev::SweepDev DevFactor::sweep_dev() const {
   dev::SweepDev S;
   S.P = plan();
-  S.dinv = dinv.p;
+  S.dinv = base ? base->dinv.p : dinv.p;
   S.phases = phases.p;
   S.nphases = nphases;
+  S.ph0 = 0;
+  S.ph1 = nphases;
   S.mtf = mt_f.p;
   S.mtb = mt_b.p;
   S.tdesc = tdesc.p;
   S.tiles = tiles.p;
   S.tile_off = tile_off.p;
-  S.Lt = Lt.p;
+  S.Lt = base ? base->Lt.p : Lt.p;
   S.sn_RB = sn_RB.p; S.sn_CB = sn_CB.p; S.sn_nrb = sn_nrb.p; S.sn_ncb = sn_ncb.p;
   S.sn_fpart = sn_fpart.p; S.sn_bpart = sn_bpart.p;
   S.fpart = fpart.p; S.bpart = bpart.p;
@@ -511,11 +542,13 @@ void DevFactor::sweep_timing(unsigned long long* ns, unsigned long long* cnt, cu
   *cnt = v[dev::SW_TCNT];
 }
 
-void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* stop) const {
+void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* stop, int seg) const {
   dev::SweepDev S = sweep_dev();
-  // the phase count must not vary between launches (the grid barrier's target is
-  // cumulative over launches): without `out` the prolongation phase runs empty
+  // without `out` the prolongation phase runs empty
   S.nphases = nphases;
+  S.ph0 = seg == 1 ? nph_a : 0;
+  S.ph1 = seg == 0 ? nph_a : nphases;
+  if (S.ph1 <= S.ph0) return;
   S.n_out = out ? n_out : 0;
   S.b = b;
   S.out = out;

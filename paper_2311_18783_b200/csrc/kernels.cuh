@@ -90,7 +90,7 @@ __global__ void k_mf_factor_level(PlanDev P, const int* __restrict__ list, const
 
 // -------------------------------------------- supernodal triangular sweeps
 // (sweep.cu) control words of a persistent sweep and its phase kinds
-enum { SW_EPOCH = 0, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
+enum { SW_EPOCH = 0 /* grid barriers completed by earlier launches */, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR, PH_CF, PH_CB };
 constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 3328;   // doubles per tile (26 KB, one TMA bulk copy)
@@ -151,6 +151,7 @@ struct SweepDev {
   const int4* phases;
   const CombDesc* cmb;
   int nphases;
+  int ph0, ph1;                  // this launch runs phases [ph0, ph1) (a segment of a sharded coarse sweep)
   const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
   const int64_t* tile_off;       // into Lt

@@ -80,3 +80,95 @@ void build_shard_plan(const HostMesh& m, const Decomp& dec, const Csr& Apat, int
 }
 
 }  // namespace mdd
+
+namespace mdd {
+
+// Subtree-to-rank mapping of the coarse factor's supernode tree:
+// grow a replicated top from the roots, splitting the costliest frontier subtree,
+// and deal the frontier subtrees to the ranks largest first (LPT); keep the
+// configuration with the smallest per-rank work max_bin + top.  Integer work,
+// deterministic on every rank.
+void split_tree(int nsn, const int32_t* parent, const int64_t* cost, int nranks, std::vector<int32_t>& owner) {
+  MDD_REQUIRE(nranks >= 1, 2, "nranks must be >= 1");
+  owner.assign(nsn, 0);
+  if (nranks == 1 || nsn == 0) return;
+  std::vector<std::vector<int32_t>> ch(nsn);
+  std::vector<int32_t> roots;
+  for (int g = 0; g < nsn; ++g) {
+    MDD_REQUIRE(parent[g] < nsn && parent[g] != g, 2, "split_tree: bad parent");
+    if (parent[g] < 0) roots.push_back(g); else ch[parent[g]].push_back(g);
+  }
+  {
+    std::vector<int32_t> order(roots);
+    for (size_t k = 0; k < order.size() && order.size() <= (size_t)nsn; ++k)
+      for (int32_t c : ch[order[k]]) order.push_back(c);
+    MDD_REQUIRE((int)order.size() == nsn, 2, "split_tree: parent array is not a forest");
+  }
+  // subtree costs, children before parents (iterative postorder)
+  std::vector<int64_t> sc(nsn, 0);
+  {
+    std::vector<std::pair<int32_t, size_t>> st;
+    for (int32_t r : roots) {
+      st.push_back({r, 0});
+      while (!st.empty()) {
+        auto& [g, k] = st.back();
+        if (k < ch[g].size()) {
+          const int32_t c = ch[g][k++];
+          st.push_back({c, 0});
+        } else {
+          sc[g] += cost[g];
+          if (parent[g] >= 0) sc[parent[g]] += sc[g];
+          st.pop_back();
+        }
+      }
+    }
+  }
+  auto by_cost = [&](int32_t a, int32_t b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; };
+  auto deal = [&](std::vector<int32_t> fr, std::vector<int32_t>& rk, int64_t& maxbin) {
+    std::sort(fr.begin(), fr.end(), by_cost);
+    std::vector<int64_t> bin(nranks, 0);
+    rk.assign(nsn, -1);
+    for (int32_t g : fr) {
+      const int b = (int)(std::min_element(bin.begin(), bin.end()) - bin.begin());
+      bin[b] += sc[g];
+      rk[g] = b;
+    }
+    maxbin = *std::max_element(bin.begin(), bin.end());
+  };
+  std::vector<int32_t> frontier(roots), top;
+  std::vector<char> is_top(nsn, 0), best_top;
+  std::vector<int32_t> rk, best_rk;
+  int64_t topcost = 0, best = INT64_MAX;
+  for (int it = 0; it <= 8 * nranks + 64; ++it) {
+    int64_t mb = 0;
+    deal(frontier, rk, mb);
+    if ((int)frontier.size() >= nranks && mb + topcost < best) {
+      best = mb + topcost;
+      best_rk = rk;
+      best_top = is_top;
+    }
+    // split the costliest frontier subtree that has children
+    int32_t s = -1;
+    for (int32_t g : frontier)
+      if (!ch[g].empty() && (s < 0 || by_cost(g, s))) s = g;
+    if (s < 0) break;
+    frontier.erase(std::find(frontier.begin(), frontier.end(), s));
+    frontier.insert(frontier.end(), ch[s].begin(), ch[s].end());
+    is_top[s] = 1;
+    topcost += cost[s];
+  }
+  MDD_REQUIRE(!best_rk.empty(), 2, "split_tree: fewer leaf subtrees than ranks");
+  // top supernodes -> -1; every other supernode -> the rank of its frontier ancestor
+  std::vector<int32_t> order;  // parents before children
+  for (int32_t r : roots) order.push_back(r);
+  for (size_t k = 0; k < order.size(); ++k)
+    for (int32_t c : ch[order[k]]) order.push_back(c);
+  MDD_REQUIRE((int)order.size() == nsn, 2, "split_tree: parent array is not a forest");
+  for (int32_t g : order) {
+    if (best_top[g]) owner[g] = -1;
+    else if (best_rk[g] >= 0) owner[g] = best_rk[g];
+    else owner[g] = owner[parent[g]];
+  }
+}
+
+}  // namespace mdd

@@ -29,4 +29,12 @@ struct ShardPlan {
 void build_shard_plan(const HostMesh& m, const Decomp& dec, const Csr& Apat, int px, int py, int pz,
                       int rank, int nranks, ShardPlan& sp);
 
+// Sharded coarse solve: subtree-to-rank mapping of a supernode tree (parent[g] <
+// 0: a root; cost[g]: the supernode's factor entries).  owner[g] = -1 for the
+// replicated top supernodes every rank sweeps, else the rank that sweeps g with
+// its whole subtree.  A top is grown from the roots by splitting the costliest
+// frontier subtree; the frontier subtrees go to the ranks largest first (LPT);
+// the configuration with the smallest max-rank subtree work + top work wins.
+void split_tree(int nsn, const int32_t* parent, const int64_t* cost, int nranks, std::vector<int32_t>& owner);
+
 }  // namespace mdd

@@ -18,8 +18,10 @@
 // processes (one GPU each), or device copies between several handles of one
 // process on one GPU (the group solve of the tests, which runs the same
 // sequence of kernels rank by rank between the exchanges).  The coarse factor
-// is replicated: every rank applies E^{-1} to the allreduced Z^T t (DESIGN.md
-// §9 states why and what the distributed coarse tree would take).
+// is set up on every rank, but E^{-1} is applied distributed:
+// each rank sweeps the subtrees of E's supernode tree split_tree gave it plus
+// the replicated top separators, with one allreduce of the frontier roots'
+// update vectors between the forward sweeps and one of the solution after.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -48,6 +50,22 @@ __global__ void k_halo_copy(int n, const int32_t* __restrict__ si, const double*
                             const int32_t* __restrict__ di, double* __restrict__ dst, int add) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) dst[di[k]] = add ? dst[di[k]] + src[si[k]] : src[si[k]];
+}
+// b[own[j]] = v[pos[own[j]]] (pos null: v[own[j]]): this rank's entries of an
+// exchange buffer whose other entries are zero
+__global__ void k_scatter_owned(int64_t nown, const int64_t* __restrict__ pos, const int32_t* __restrict__ own,
+                                const double* __restrict__ v, double* __restrict__ b) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nown) {
+    const int32_t k = own[j];
+    b[k] = v[pos ? pos[k] : k];
+  }
+}
+// v[pos[k]] = b[k]
+__global__ void k_unpack_all(int64_t n, const int64_t* __restrict__ pos, const double* __restrict__ b,
+                             double* __restrict__ v) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) v[pos[k]] = b[k];
 }
 __global__ void k_vadd(int64_t n, const double* __restrict__ a, double* __restrict__ acc) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -114,6 +132,18 @@ struct ShardState {
   DBuf<int32_t> send_idx, recv_idx;
   DBuf<double> sbuf, rbuf, acc;
   DBuf<double> x, r, p, q, z, w, t, u;   // p, r, w: local layout (n_loc); the rest owned (n_loc for simplicity)
+  // distributed coarse solve (nranks > 1): this rank's view of the replicated
+  // coarse factor sweeping its subtrees (segment A) and the replicated top
+  // (segment B); between the two, the update vectors of the frontier subtree
+  // roots (ux_pos, the same list on every rank; this rank fills ux_own) are
+  // summed over the ranks; after B, the coarse solution (y_own: the positions
+  // this rank provides) likewise
+  bool dist_coarse = false;
+  DevFactor crs;
+  DBuf<int64_t> ux_pos;
+  DBuf<int32_t> ux_own, y_own;
+  DBuf<double> ubuf, ybuf;
+  int64_t n_ux = 0, n_ux_own = 0, n_y_own = 0, top_entries = 0;
   ncclComm_t comm = nullptr;
   ~ShardState() {
     if (comm) nccl().CommDestroy(comm);
@@ -238,13 +268,60 @@ void shard_setup(mdd_solver* H, int rank, int nranks) {
     }
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
+  // ---- distributed coarse solve: subtree-to-rank split of E's supernode tree
+  if (H->has_coarse && nranks > 1 && !getenv("MDD_SHARD_COARSE_REPLICATED")) {
+    const FactorPlan& cf = H->crs.fp;
+    std::vector<int64_t> cost(cf.nsn);
+    for (int g = 0; g < cf.nsn; ++g) {
+      const int64_t nc = cf.sn_ncol[g], no = cf.sn_noff[g];
+      cost[g] = nc * (nc + 1) / 2 + nc * no;
+    }
+    std::vector<int32_t> owner;
+    split_tree(cf.nsn, cf.sn_parent.data(), cost.data(), nranks, owner);
+    S->crs.fp = cf;
+    std::vector<int64_t>().swap(S->crs.fp.asm_src);  // assembly maps: factorisation only
+    std::vector<int32_t>().swap(S->crs.fp.asm_pos);
+    S->crs.base = &H->crs;
+    S->crs.name = "coarse_shard" + std::to_string(rank);
+    S->crs.role.assign(cf.nsn, 0);
+    for (int g = 0; g < cf.nsn; ++g) S->crs.role[g] = owner[g] < 0 ? 2 : owner[g] == rank ? 1 : 0;
+    S->crs.upload();
+    // update vectors of the frontier subtree roots (a non-top supernode whose
+    // parent is top): every rank's list, in supernode order; this rank's entries
+    std::vector<int64_t> ux;
+    std::vector<int32_t> uo, yo;
+    for (int g = 0; g < cf.nsn; ++g) {
+      const int pg = cf.sn_parent[g];
+      if (owner[g] < 0 || pg < 0 || owner[pg] >= 0) continue;
+      for (int a = 0; a < cf.sn_noff[g]; ++a) {
+        if (owner[g] == rank) uo.push_back((int32_t)ux.size());
+        ux.push_back(cf.sn_uptr[g] + a);
+      }
+    }
+    // coarse positions this rank provides: its subtrees' columns; rank 0 also the top's
+    for (int g = 0; g < cf.nsn; ++g)
+      if (owner[g] == rank || (owner[g] < 0 && rank == 0))
+        for (int c = 0; c < cf.sn_ncol[g]; ++c) yo.push_back((int32_t)(cf.sn_col0[g] + c));
+    S->top_entries = 0;
+    for (int g = 0; g < cf.nsn; ++g)
+      if (owner[g] < 0) S->top_entries += cost[g];
+    S->n_ux = (int64_t)ux.size();
+    S->n_ux_own = (int64_t)uo.size();
+    S->n_y_own = (int64_t)yo.size();
+    S->ux_pos.upload(ux.empty() ? std::vector<int64_t>{0} : ux);
+    S->ux_own.upload(uo.empty() ? std::vector<int32_t>{0} : uo);
+    S->y_own.upload(yo.empty() ? std::vector<int32_t>{0} : yo);
+    S->ubuf.alloc(std::max<int64_t>(S->n_ux, 1));
+    S->ybuf.alloc(std::max<int64_t>(H->n0, 1));
+    S->dist_coarse = true;
+  }
   // ---- exchange lists and vectors
   S->send_idx.upload(P.send_idx.empty() ? std::vector<int32_t>{0} : P.send_idx);
   S->recv_idx.upload(P.recv_idx.empty() ? std::vector<int32_t>{0} : P.recv_idx);
   const size_t nbuf = std::max<size_t>(std::max(P.send_idx.size(), P.recv_idx.size()), 1);
   S->sbuf.alloc(nbuf);
   S->rbuf.alloc(nbuf);
-  S->acc.alloc(std::max<int64_t>(H->n0, 8) + 8);
+  S->acc.alloc(std::max<int64_t>(std::max<int64_t>(H->n0, S->n_ux), 8) + 8);
   for (DBuf<double>* b : {&S->x, &S->r, &S->p, &S->q, &S->z, &S->w, &S->t, &S->u}) {
     b->alloc(std::max(S->n_loc, 1));
     b->zero(s);
@@ -368,10 +445,42 @@ struct ShardSolve {
       ++launches;
     });
     T.allreduce(M, [](Member& m) { return m.h->xc.p; }, M[0].h->n0, st);
+    const bool dist = M[0].s->dist_coarse;
+    if (dist) {
+      // E^{-1} distributed: each rank sweeps its subtrees forward (segment A), the
+      // frontier roots' update vectors are summed over the ranks, every rank sweeps
+      // the top forward and backward and its subtrees backward (segment B), and
+      // the ranks' parts of the solution are summed (zeros elsewhere: exact)
+      each([&](Member& m) {
+        m.s->crs.sweep(m.h->xc.p, nullptr, st, m.h->state.p, 0);
+        CUDA_CHECK(cudaMemsetAsync(m.s->ubuf.p, 0, m.s->ubuf.n * sizeof(double), st));
+        const int64_t no = m.s->n_ux_own;
+        if (no) k_scatter_owned<<<nblk(no, 256), 256, 0, st>>>(no, m.s->ux_pos.p, m.s->ux_own.p, m.s->crs.upd.p,
+                                                               m.s->ubuf.p);
+        launches += 2;
+      });
+      if (M[0].s->n_ux) {
+        T.allreduce(M, [](Member& m) { return m.s->ubuf.p; }, M[0].s->n_ux, st);
+        each([&](Member& m) {
+          k_unpack_all<<<nblk(m.s->n_ux, 256), 256, 0, st>>>(m.s->n_ux, m.s->ux_pos.p, m.s->ubuf.p, m.s->crs.upd.p);
+          ++launches;
+        });
+      }
+      each([&](Member& m) {
+        m.s->crs.sweep(m.h->xc.p, nullptr, st, m.h->state.p, 1);
+        CUDA_CHECK(cudaMemsetAsync(m.s->ybuf.p, 0, m.s->ybuf.n * sizeof(double), st));
+        if (m.s->n_y_own)
+          k_scatter_owned<<<nblk(m.s->n_y_own, 256), 256, 0, st>>>(m.s->n_y_own, nullptr, m.s->y_own.p,
+                                                                  m.s->crs.xb.p, m.s->ybuf.p);
+        launches += 2;
+      });
+      T.allreduce(M, [](Member& m) { return m.s->ybuf.p; }, M[0].h->n0, st);
+    }
     each([&](Member& m) {
-      m.h->crs.sweep(m.h->xc.p, nullptr, st, m.h->state.p);
+      if (!dist) m.h->crs.sweep(m.h->xc.p, nullptr, st, m.h->state.p);
+      const double* y = dist ? m.s->ybuf.p : m.h->crs.xb.p;
       dev::k_spmv8<<<m.h->nparts, 256, 0, st>>>(m.s->n_own, m.s->Z_ptr.p, m.s->Z_idx.p, m.s->Z_val.p,
-                                               m.h->crs.xb.p, nullptr, m.s->u.p, nullptr, nullptr, m.h->state.p,
+                                               y, nullptr, m.s->u.p, nullptr, nullptr, m.h->state.p,
                                                mdd_solver::rnone());
       double* o = out(m);
       const double* a = add ? add(m) : nullptr;
@@ -474,6 +583,7 @@ struct ShardSolve {
     for (auto& m : M) {
       m.s->loc.check_abort(st);
       if (m.h->has_coarse) m.h->crs.check_abort(st);
+      if (m.s->dist_coarse) m.s->crs.check_abort(st);
     }
     *iters = hs[ST_ITERS];
     *relres = M[0].h->host_S[S_REL];
@@ -515,9 +625,12 @@ int mdd_shard_setup(mdd_handle h, int rank, int nranks) {
 
 int mdd_shard_info(mdd_handle h, int64_t* out, int count) {
   if (!h || !out || !h->shard) { mdd::set_last_error("null argument or no shard"); return MDD_ERR_ARG; }
-  const int64_t v[4] = {h->shard->n_own, h->shard->n_loc, (int64_t)h->shard->plan.subs.size(),
-                        h->shard->loc.fp.factor_nnz()};
-  for (int k = 0; k < count && k < 4; ++k) out[k] = v[k];
+  const mdd::ShardState& S = *h->shard;
+  const int64_t v[8] = {S.n_own, S.n_loc, (int64_t)S.plan.subs.size(), S.loc.fp.factor_nnz(),
+                        S.dist_coarse ? 1 : 0,
+                        S.dist_coarse ? S.crs.swept_entries : (h->has_coarse ? h->crs.fp.factor_nnz() : 0),
+                        S.top_entries, S.n_ux};
+  for (int k = 0; k < count && k < 8; ++k) out[k] = v[k];
   return MDD_OK;
 }
 

@@ -33,7 +33,8 @@
 // in a fixed order (one barrier instead of a publishing atomic and a deferred
 // combine per group: those cost ~2 us of CTA time per group, measured on c4) --
 // every reduction is bit-reproducible and independent of the grid size.  The
-// barrier counter is cumulative across launches (epoch); a barrier wait that
+// barrier counter is cumulative across launches (SW_EPOCH: the barriers of the
+// earlier launches, so launches may run different phase ranges); a barrier wait that
 // exceeds kSpinTimeoutNs raises an abort flag reported by the host.
 #include "kernels.cuh"
 
@@ -439,7 +440,9 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   __shared__ int s_tinfo[kStages];
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
-  const unsigned long long cur = S.ctl[SW_EPOCH] + 1;
+  // barriers of earlier launches (cumulative counter: the targets of this launch
+  // continue from them)
+  const unsigned long long base = S.ctl[SW_EPOCH];
   const unsigned long long grid = gridDim.x;
   if (tid == 0) {
     atomicMin(&S.ctl[SW_T0], globaltimer());
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   const size_t gthreads = (size_t)gridDim.x * kSweepThreads;
   const size_t gtid = (size_t)blockIdx.x * kSweepThreads + tid;
 
-  for (int ph = 0; ph < S.nphases; ++ph) {
+  for (int ph = S.ph0; ph < S.ph1; ++ph) {
     const int4 PH = S.phases[ph];
     const int kind = PH.x;
     const unsigned long long t_ph = (S.trace && tid == 0) ? globaltimer() : 0ull;
@@ -771,15 +774,14 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       tr[6] = t_body;
       tr[7] = t_tasks;
     }
-    if (ph + 1 < S.nphases)
-      grid_barrier(S.ctl, ((cur - 1) * (unsigned long long)(S.nphases - 1) + ph + 1) * grid);
+    if (ph + 1 < S.ph1) grid_barrier(S.ctl, (base + (unsigned long long)(ph - S.ph0) + 1) * grid);
   }
   if (blockIdx.x == 0 && tid == 0) {
     // every CTA read the epoch before the first barrier
     S.ctl[SW_TSUM] += globaltimer() - S.ctl[SW_T0];
     S.ctl[SW_TCNT] += 1;
     S.ctl[SW_T0] = ~0ull;
-    S.ctl[SW_EPOCH] = cur;
+    S.ctl[SW_EPOCH] = base + (unsigned long long)(S.ph1 - S.ph0 - 1);
     __threadfence();
   }
 }

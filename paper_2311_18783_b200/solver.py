@@ -52,6 +52,20 @@ def shard_array(w, rank: int, nranks: int, name: str) -> np.ndarray:
     return out
 
 
+def tree_split(parent, cost, nranks: int) -> np.ndarray:
+    """Host-only subtree-to-rank mapping of a supernode tree (mdd_tree_split):
+    -1 = replicated top supernode, else the rank sweeping it with its subtree."""
+    par = np.ascontiguousarray(parent, dtype=np.int32)
+    cst = np.ascontiguousarray(cost, dtype=np.int64)
+    if par.shape != cst.shape or par.ndim != 1:
+        raise ValueError("parent and cost must be 1-D arrays of equal length")
+    out = np.empty(len(par), np.int32)
+    L.check(L.lib().mdd_tree_split(len(par), par.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   cst.ctypes.data_as(C.POINTER(C.c_int64)), int(nranks),
+                                   out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
 def _ptr(t, n=None, device=None) -> int:
     """Device pointer of a contiguous float64 CUDA tensor of n elements on the
     handle's device (the C ABI reads / writes exactly n doubles)."""
@@ -234,10 +248,12 @@ class MaxwellDD:
     def shard_setup(self, rank: int, nranks: int):
         """This handle becomes rank `rank` of a sharded solve (mdd_shard_setup)."""
         L.check(L.lib().mdd_shard_setup(self._h, rank, nranks))
-        out = (C.c_int64 * 4)()
-        L.check(L.lib().mdd_shard_info(self._h, out, 4))
+        out = (C.c_int64 * 8)()
+        L.check(L.lib().mdd_shard_info(self._h, out, 8))
         self.shard = {"rank": rank, "nranks": nranks, "n_own": int(out[0]), "n_local": int(out[1]),
-                      "subdomains": int(out[2]), "factor_nnz": int(out[3])}
+                      "subdomains": int(out[2]), "factor_nnz": int(out[3]), "coarse_distributed": bool(out[4]),
+                      "coarse_swept_nnz": int(out[5]), "coarse_top_nnz": int(out[6]),
+                      "coarse_exchange": int(out[7])}
         self.owned = shard_array(self.w, rank, nranks, "owned")
         return self.shard
 
