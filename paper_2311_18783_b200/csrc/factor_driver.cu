@@ -394,6 +394,16 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   auto fused = [&](const std::vector<int>& lev, int l) {
     return lev[l + 1] - lev[l] <= fuse_tasks * plan_grid;
   };
+  // a combine phase goes one CTA per item (bit 1) when its items are few (<= 2 per
+  // CTA) and their partial chains long (>= 8): a warp per item would walk ntl / 4
+  // dependent loads while most of the grid idles
+  auto cta_comb = [&](const std::vector<int>& lev, int l) {
+    int mx = 0;
+    for (int k = lev[l]; k < lev[l + 1]; ++k) mx = std::max(mx, cm[k].ntl);
+    for (int k = lev[l]; k < lev[l + 1]; ++k)
+      MDD_REQUIRE(cm[k].m <= 2 * dev::kVecMax / 4, 5, "combine item wider than its reduction slot");
+    return (lev[l + 1] - lev[l] <= 2 * plan_grid && mx >= 8) ? 2 : 0;
+  };
   std::vector<int4> ph;
   nph_a = 0;
   for (int l = 0; l < NL; ++l) {
@@ -402,14 +412,14 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
     if (!fz) ph.push_back(make_int4(dev::PH_GF, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MF, lev_f[l], lev_f[l + 1], fz ? 1 : 0));
     // the level's 2-D partial sums, added before any later phase reads xf / upd
-    if (cmf[l + 1] > cmf[l]) ph.push_back(make_int4(dev::PH_CF, cmf[l], cmf[l + 1], fz ? 1 : 0));
+    if (cmf[l + 1] > cmf[l]) ph.push_back(make_int4(dev::PH_CF, cmf[l], cmf[l + 1], (fz ? 1 : 0) | cta_comb(cmf, l)));
   }
   if (nlev_a == NL && nlev_a > 0) nph_a = (int)ph.size();
   for (int l = NL - 1; l >= 0; --l) {
     const bool fz = fused(lev_b, l);
     if (!fz) ph.push_back(make_int4(dev::PH_GB, (int)lev_row[l], (int)lev_row[l + 1], 0));
     ph.push_back(make_int4(dev::PH_MB, lev_b[l], lev_b[l + 1], fz ? 1 : 0));
-    if (cmb_lev[l + 1] > cmb_lev[l]) ph.push_back(make_int4(dev::PH_CB, cmb_lev[l], cmb_lev[l + 1], 0));
+    if (cmb_lev[l + 1] > cmb_lev[l]) ph.push_back(make_int4(dev::PH_CB, cmb_lev[l], cmb_lev[l + 1], cta_comb(cmb_lev, l)));
   }
   if (prolong_n > 0) {
     ph.push_back(make_int4(dev::PH_PR, 0, prolong_n, 0));
@@ -486,6 +496,7 @@ dev::SweepDev DevFactor::sweep_dev() const {
   S.nphases = nphases;
   S.ph0 = 0;
   S.ph1 = nphases;
+  S.flags = 0;
   S.mtf = mt_f.p;
   S.mtb = mt_b.p;
   S.tdesc = tdesc.p;
@@ -546,6 +557,8 @@ void DevFactor::sweep(const double* b, double* out, cudaStream_t s, const int* s
   dev::SweepDev S = sweep_dev();
   // without `out` the prolongation phase runs empty
   S.nphases = nphases;
+  const char* fl = getenv("MDD_SWEEP_FLAGS");  // per launch (experiments toggle it)
+  S.flags = fl ? atoi(fl) : 0;
   S.ph0 = seg == 1 ? nph_a : 0;
   S.ph1 = seg == 0 ? nph_a : nphases;
   if (S.ph1 <= S.ph0) return;

@@ -92,6 +92,9 @@ __global__ void k_mf_factor_level(PlanDev P, const int* __restrict__ list, const
 // (sweep.cu) control words of a persistent sweep and its phase kinds
 enum { SW_EPOCH = 0 /* grid barriers completed by earlier launches */, SW_BAR, SW_ABORT, SW_T0, SW_TSUM, SW_TCNT, SW_COUNT };
 enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR, PH_CF, PH_CB };
+// SweepDev::flags (experiments, env MDD_SWEEP_FLAGS read per launch; 0 = default;
+// measured on c4: one CTA per combine item, coarse sweep 3.78 -> 3.65 ms)
+enum { SWF_NO_CTA_COMBINE = 2 };
 constexpr int kSweepThreads = 256;
 constexpr int kTileMax = 3328;   // doubles per tile (26 KB, one TMA bulk copy)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
@@ -147,11 +150,13 @@ struct SweepDev {
   const MTaskDesc* mtb;
   // phases {kind, a, b, w}: G: rows [a, b) of vb; M: mtask [a, b), w = 1 when the
   // level's gather is fused into its tasks (no G phase before it); C: combine
-  // items [a, b), w = 1 when the level's t rows are not in vb (fused); PR
+  // items [a, b), w bit 0 when the level's t rows are not in vb (fused), bit 1
+  // one CTA per item (few items, long partial chains); PR
   const int4* phases;
   const CombDesc* cmb;
   int nphases;
   int ph0, ph1;                  // this launch runs phases [ph0, ph1) (a segment of a sharded coarse sweep)
+  int flags;                     // SWF_* (experiments)
   const int4* tdesc;             // {tile, bytes, offset lo, offset hi}
   const int4* tiles;             // {supernode, row block, column block, 0}
   const int64_t* tile_off;       // into Lt

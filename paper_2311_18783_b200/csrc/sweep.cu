@@ -94,8 +94,9 @@ __device__ __forceinline__ double gather_w(const SweepDev& S, long long q) {
   return di != 0.0 ? __ldcg(S.xf + w) / di : 0.0;
 }
 
-// grid-wide barrier over co-resident CTAs (cumulative counter, no reset)
-__device__ void grid_barrier(unsigned long long* ctl, unsigned long long target) {
+// grid-wide barrier over co-resident CTAs (cumulative counter, no reset); *abort
+// (shared) receives the abort flag as thread 0 saw it, uniform across the CTA
+__device__ void grid_barrier(unsigned long long* ctl, unsigned long long target, int* abort) {
   // bar.sync orders the CTA's writes before thread 0's release add; thread 0's
   // acquire load and the second bar.sync order every later read after the other
   // CTAs' writes (release/acquire at gpu scope, no full fence)
@@ -116,6 +117,7 @@ __device__ void grid_barrier(unsigned long long* ctl, unsigned long long target)
         }
       }
     }
+    *abort = *(volatile unsigned long long*)&ctl[SW_ABORT] != 0;
   }
   __syncthreads();
 }
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   __shared__ __align__(8) uint64_t mbar[kStages];
   __shared__ __align__(16) MTaskDesc s_desc[kDescRing];
   __shared__ int s_tinfo[kStages];
+  __shared__ int s_abort;  // the abort flag as of the last grid barrier (CTA-uniform)
   const int tid = threadIdx.x;
   if (S.stop && *S.stop) return;  // PCG already stopped: the whole sweep is a no-op
   // barriers of earlier launches (cumulative counter: the targets of this launch
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
   if (tid == 0) {
     atomicMin(&S.ctl[SW_T0], globaltimer());
     for (int q = 0; q < kStages; ++q) mbar_init(&mbar[q]);
+    s_abort = *(volatile unsigned long long*)&S.ctl[SW_ABORT] != 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -509,9 +513,52 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       // (backward): one warp per block, each lane two outputs (o, o + 32) with four
       // partial chains each (eight loads in flight); fixed order, grid-independent:
       // sum = (a0 + a1) + (a2 + a3), a_k = the partials q = k mod 4 in index order
-      const bool cf = kind == PH_CF, fz = PH.w != 0;
+      const bool cf = kind == PH_CF, fz = (PH.w & 1) != 0;
       const int lane = tid & 31;
       const size_t nw = (size_t)gridDim.x * kWarps;
+      if ((PH.w & 2) && !(S.flags & SWF_NO_CTA_COMBINE)) {
+        // few items with long partial chains (the upper levels' big supernodes):
+        // one CTA per item, warp w sums the partials [w ntl / 8, (w+1) ntl / 8)
+        // (four chains, as below), then the eight warp sums are added in warp
+        // order -- fixed, grid-independent
+        const int warp = tid >> 5;
+        double* const wred = sm;  // the tile ring is idle in a C phase
+        for (size_t it = (size_t)PH.y + blockIdx.x; it < (size_t)PH.z; it += gridDim.x) {
+          const CombDesc C = S.cmb[it];
+          const double* pb = (cf ? S.fpart : S.bpart) + C.comb;
+          const int q0 = (warp * C.ntl) / kWarps, q1 = ((warp + 1) * C.ntl) / kWarps;
+          for (int o = lane; o < C.m; o += 64) {
+            const bool two = o + 32 < C.m;
+            double a[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
+            int q = q0;
+            for (; q + 4 <= q1; q += 4) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                a[k] += __ldcg(pb + (i64)(q + k) * C.ld + o);
+                if (two) e[k] += __ldcg(pb + (i64)(q + k) * C.ld + o + 32);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (q + k < q1) {
+                a[k] += __ldcg(pb + (i64)(q + k) * C.ld + o);
+                if (two) e[k] += __ldcg(pb + (i64)(q + k) * C.ld + o + 32);
+              }
+            wred[warp * 2 * kVecMax / 4 + o] = (a[0] + a[1]) + (a[2] + a[3]);
+            if (two) wred[warp * 2 * kVecMax / 4 + o + 32] = (e[0] + e[1]) + (e[2] + e[3]);
+          }
+          __syncthreads();
+          for (int o = tid; o < C.m; o += kSweepThreads) {
+            double sum = 0.0;
+            for (int w = 0; w < kWarps; ++w) sum += wred[w * 2 * kVecMax / 4 + o];
+            const int r = C.first + o;
+            if (!cf) S.xb[C.col0 + r] = sum;
+            else if (r < C.nc) S.xf[C.col0 + r] = sum;
+            else S.upd[C.uptr + (r - C.nc)] = (fz ? gather_t(S, C.vo + r) : __ldcg(S.vb + C.vo + r)) - sum;
+          }
+          __syncthreads();
+        }
+      } else
       for (size_t it = (size_t)PH.y + (size_t)blockIdx.x * kWarps + (tid >> 5); it < (size_t)PH.z; it += nw) {
         const CombDesc C = S.cmb[it];
         const double* pb = (cf ? S.fpart : S.bpart) + C.comb;
@@ -549,7 +596,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
         for (i64 k = S.pro_ptr[e]; k < S.pro_ptr[e + 1]; ++k) s += __ldcg(S.xb + S.pro_pos[k]);
         S.out[e] = s;
       }
-    } else if (!*(volatile unsigned long long*)&S.ctl[SW_ABORT]) {
+    } else if (!s_abort) {
       // ---------------------------------------------- M phase: tiles.  Tasks are
       // sorted largest first and dealt to the CTAs in snake order (no atomics);
       // every per-task quantity comes from one packed descriptor.
@@ -774,7 +821,7 @@ __global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
       tr[6] = t_body;
       tr[7] = t_tasks;
     }
-    if (ph + 1 < S.ph1) grid_barrier(S.ctl, (base + (unsigned long long)(ph - S.ph0) + 1) * grid);
+    if (ph + 1 < S.ph1) grid_barrier(S.ctl, (base + (unsigned long long)(ph - S.ph0) + 1) * grid, &s_abort);
   }
   if (blockIdx.x == 0 && tid == 0) {
     // every CTA read the epoch before the first barrier

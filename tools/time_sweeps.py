@@ -41,6 +41,21 @@ if "--nocompute" in sys.argv:   # experiment build (MDD_NVCC_FLAGS=-DMDD_DEBUG_N
                       "with_math_coarse_ms": timed(lambda: G.apply_coarse_inverse(v0, y0))}))
     assert _lib.lib().mdd_debug_set_nocompute(1) == 0
 bm = G.bytes_model()
+if "--flags" in sys.argv:   # MDD_SWEEP_FLAGS variants (2: one warp per combine item, the round-1 scheme)
+    cb = 16 * G.info["coarse_factor_nnz"] + 16 * n0
+    ref = {}
+    for fl in (2, 0, 2, 0):
+        os.environ["MDD_SWEEP_FLAGS"] = str(fl)
+        tl = timed(lambda: G.apply_local(v, y))
+        tc = timed(lambda: G.apply_coarse_inverse(v0, y0))
+        out = (y.clone(), y0.clone())
+        if fl not in ref:
+            ref[fl] = out
+        same = {k: float(((out[0] - r[0]).norm() / r[0].norm()).item()) for k, r in ref.items()}
+        same0 = {k: float(((out[1] - r[1]).norm() / r[1].norm()).item()) for k, r in ref.items()}
+        print(json.dumps({"flags": fl, "local_ms": tl, "local_GBs": bm["local"] / tl / 1e6, "coarse_ms": tc,
+                          "coarse_GBs": cb / tc / 1e6, "local_vs": same, "coarse_vs": same0}), flush=True)
+    os.environ.pop("MDD_SWEEP_FLAGS")
 tl = timed(lambda: G.apply_local(v, y))
 tc = timed(lambda: G.apply_coarse_inverse(v0, y0))
 cb = 16 * G.info["coarse_factor_nnz"] + 16 * n0
