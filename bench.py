@@ -71,6 +71,11 @@ def parse():
     ap.add_argument("--variant", default="as2_coarse_start",
                     choices=["as2_coarse_start", "as2", "additive", "as1"])
     ap.add_argument("--maxit", type=int, default=2000)
+    # replicas: every rank its own copy of the workload (weak scaling, the default);
+    # sharded: ONE copy of the workload, its subdomains sharded over the ranks (strong
+    # scaling): halo exchanges and the pTq / |r|^2 / rTz / coarse allreduces over NCCL
+    # (sharded.cu); the setup is replicated on every rank
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
     return ap.parse_args()
 
 
@@ -198,6 +203,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.mode == "sharded":
+        run_sharded(args, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     w = workloads.make(args.config)
     t0 = time.perf_counter()
@@ -366,6 +376,120 @@ def main():
     G.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sharded(args, rank, world, local):
+    """One copy of the workload, its subdomains sharded over the ranks (strong
+    scaling; mdd_shard_setup / mdd_shard_solve): per iteration the forward halos of
+    p, r and w, the reverse halo of the local solves, the allreduces of pTq, |r|^2,
+    rTz, Z^T r and the two exchanges of the distributed coarse solve go over NCCL.
+    The setup (and E's factor, swept by subtree) is replicated on every rank.
+    value = n * iterations / max-over-ranks device time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2311_18783_b200 import MaxwellDD
+
+    w = workloads.make(args.config)
+    t0 = time.perf_counter()
+    G = MaxwellDD(w, device=local, variant=args.variant)
+    sh = G.shard_setup(rank, world)
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.Stream()
+    G.set_stream(stream)
+    uid = [bytes(torch.cuda.nccl.unique_id()) if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    G.shard_nccl_init(uid[0])
+    n, n_own = G.n, sh["n_own"]
+    f_host = workloads.rhs(n, w.f_seed)[G.owned]
+    f = torch.as_tensor(f_host, device="cuda")
+    x = torch.empty(n_own, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step(host=False):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        it, relres, ok = G.shard_solve(f, x, tol=TOL, maxit=args.maxit)
+        e1.record(stream)
+        e1.synchronize()
+        assert ok, f"sharded PCG did not converge (relres {relres})"
+        return e0.elapsed_time(e1), it
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    t_ms, it = 0.0, 0
+    for _ in range(args.steps):
+        ms, it = step()
+        t_ms += ms
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    step_ms = t_ms / args.steps
+    # every rank reports the same iterations; the job's work is n * it once
+    step_ms_max, _ = reduce_over_ranks(step_ms, 0.0, world, "cuda")
+    value = n * it / (step_ms_max / 1e3)
+    # e2e: this rank's part of f from pinned host memory, its part of x back
+    import ctypes as C
+    from paper_2311_18783_b200 import _lib as L
+    fp = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
+    fp.numpy()[:] = f_host
+    xp = torch.empty(n_own, dtype=torch.float64, pin_memory=True)
+    e2e_ms = 0.0
+    for _ in range(max(1, args.steps)):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        itc, rel = C.c_int(0), C.c_double(0.0)
+        rc = L.lib().mdd_shard_solve(G._h, fp.data_ptr(), xp.data_ptr(), TOL, args.maxit, 1,
+                                     C.byref(itc), C.byref(rel))
+        assert rc == L.MDD_OK, rc
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+    e2e_ms_max, _ = reduce_over_ranks(e2e_ms / max(1, args.steps), 0.0, world, "cuda")
+    info = G._info()
+    peak, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+            src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        pass
+    # the whole job's algorithmic bytes per iteration (the single-GPU model: the
+    # replicated top of E is counted once) against world x the measured HBM peak
+    bm = G.bytes_model()
+    gbs = bm["iteration"] * it / (step_ms_max / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n_dofs": n, "subdomains": info["nsub"], "n0_coarse": info["n0"],
+                   "geneo_vectors": info["ngeneo"], "iterations": it, "tol": TOL, "gamma": w.gamma,
+                   "variant": args.variant, "parallelism": f"sharded x{world} (setup replicated)",
+                   "l2": "flushed between steps (256 MB write)"},
+        "iterations": it, "setup_s": setup_s,
+        "shard_rank0": {k: v for k, v in sh.items()},
+        "roofline": {"bound": "hbm", "kernel": "whole PCG iteration (all ranks)", "achieved": gbs,
+                     "peak": peak * world, "unit": "GB/s", "frac": gbs / (peak * world), "traffic": None,
+                     "peak_source": src + f" x {world} GPUs", "bytes_per_iteration": bm["iteration"]},
+        "e2e": {"value": n * it / (e2e_ms_max / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n_own,
+                "d2h_bytes_per_step": 8 * n_own},
+        "gpu_launches": int(G.last_launches()) * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    G.close()
 
 
 def roofline(G, sweep_ms, in_step, csweep_ms=None, cin_step=(0.0, 0), total_ms=None, cfg=None):

@@ -3,6 +3,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <queue>
 
 #include <cublas_v2.h>
 #include <cusolverDn.h>
@@ -207,6 +210,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   std::vector<dev::MTaskDesc> mtf, mtb;
   std::vector<int4> td;
   std::vector<int> lev_f(NL + 1, 0), lev_b(NL + 1, 0);
+  std::vector<int> nreal[2] = {std::vector<int>(NL, 0), std::vector<int>(NL, 0)};  // tasks without padding
   // combine items (one per row block / column block of a 2-D supernode) per level
   std::vector<dev::CombDesc> cm;
   std::vector<int> cmf(NL + 1, 0), cmb_lev(NL + 1, 0);
@@ -346,17 +350,69 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
       std::vector<Cand> lt;
       int64_t best = INT64_MAX;
       const int only_group = getenv("MDD_GROUP") ? atoi(getenv("MDD_GROUP")) : 0;  // debug
+      // MDD_DEAL=lpt: instead of the snake over the sorted tasks, each task (largest
+      // first) goes to the CTA with the least load so far (longest-processing-time
+      // rule); the kernel still deals position r * grid + q to CTA q (r even) or
+      // grid - 1 - q (r odd), so the tasks are LAID OUT in that order, a CTA with
+      // fewer tasks than rounds padded at its tail with empty tasks (no tiles, no
+      // rows).  Which CTA runs a task never changes a result.
+      // (a debug grid smaller than the planned one would deal padding between a
+      // CTA's real tasks -- their vector slots assume none -- so it keeps the snake)
+      const bool lpt = getenv("MDD_DEAL") && !strcmp(getenv("MDD_DEAL"), "lpt") && sweep_grid == plan_grid;
+      std::vector<std::vector<int>> own_best;
       for (int kGroup : {4, 2, 1}) {
         if (only_group && kGroup != only_group) continue;
         std::vector<Cand> c = build_level(kGroup);
         std::vector<int64_t> load(plan_grid, 0);
-        for (size_t i = 0; i < c.size(); ++i) {
-          const int64_t r = (int64_t)i / plan_grid, q = (int64_t)i % plan_grid;
-          load[(r & 1) ? plan_grid - 1 - q : q] += c[i].bytes + kTaskCostBytes;
+        std::vector<std::vector<int>> own;
+        if (lpt) {
+          own.resize(plan_grid);
+          // (load, cta) min-heap; ties to the lowest CTA index
+          std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>,
+                              std::greater<std::pair<int64_t, int>>> pq;
+          for (int q = 0; q < plan_grid; ++q) pq.push({0, q});
+          for (size_t i = 0; i < c.size(); ++i) {
+            auto [ld, q] = pq.top();
+            pq.pop();
+            own[q].push_back((int)i);
+            load[q] = ld + c[i].bytes + kTaskCostBytes;
+            pq.push({load[q], q});
+          }
+        } else {
+          for (size_t i = 0; i < c.size(); ++i) {
+            const int64_t r = (int64_t)i / plan_grid, q = (int64_t)i % plan_grid;
+            load[(r & 1) ? plan_grid - 1 - q : q] += c[i].bytes + kTaskCostBytes;
+          }
         }
         const int64_t mk = *std::max_element(load.begin(), load.end());
-        if (mk < best) { best = mk; lt.swap(c); }
+        if (getenv("MDD_PLAN_STATS")) {
+          int64_t sum = 0;
+          for (int64_t v : load) sum += v;
+          fprintf(stderr, "  [deal %s dir %d level %d group %d] tasks %zu max load %lld mean %lld\n", name.c_str(), dir,
+                  l, kGroup, c.size(), (long long)mk, (long long)(sum / plan_grid));
+        }
+        if (mk < best) { best = mk; lt.swap(c); own_best.swap(own); }
         if (getenv("MDD_FIXED_GROUP")) break;  // debug: always groups of 4
+      }
+      nreal[dir][l] = (int)lt.size();
+      if (lpt && !lt.empty()) {
+        size_t rounds = 0;
+        for (auto& o : own_best) rounds = std::max(rounds, o.size());
+        std::vector<Cand> laid;
+        laid.reserve(rounds * (size_t)plan_grid);
+        size_t last = 0;
+        for (size_t r = 0; r < rounds; ++r)
+          for (int q = 0; q < plan_grid; ++q) {
+            const int b = (r & 1) ? plan_grid - 1 - q : q;
+            if (r < own_best[b].size()) {
+              laid.push_back(std::move(lt[own_best[b][r]]));
+              last = laid.size();
+            } else {
+              laid.push_back(Cand{});  // an empty task: k0 == k1, nr == 0, vn == 0
+            }
+          }
+        laid.resize(last);
+        lt.swap(laid);
       }
       if (dir == 0) cmf[l] = (int)cm.size(); else cmb_lev[l] = (int)cm.size();
       for (auto& c : lt) {
@@ -392,7 +448,7 @@ void DevFactor::upload(int prolong_n, const int64_t* pro_ptr_dev, const int32_t*
   // flat gather (many rows, many tasks per CTA).  Same sums in the same order.
   const int fuse_tasks = getenv("MDD_FUSE_TASKS") ? atoi(getenv("MDD_FUSE_TASKS")) : 2;
   auto fused = [&](const std::vector<int>& lev, int l) {
-    return lev[l + 1] - lev[l] <= fuse_tasks * plan_grid;
+    return nreal[&lev == &lev_f ? 0 : 1][l] <= fuse_tasks * plan_grid;
   };
   // a combine phase goes one CTA per item (bit 1) when its items are few (<= 2 per
   // CTA) and their partial chains long (>= 8): a warp per item would walk ntl / 4

@@ -40,6 +40,12 @@ CASES_LITERAL = {
     "c3-lit-12": lambda: workloads.make("c3", n=12, p=2, contrast=1e2, gamma=1.0),
     "c4-lit-12": lambda: workloads.make("c4", m=12, q=2, contrast=1e2, gamma=1.0),
     "c4-lit-x2": lambda: workloads.make("c4", m=8, q=2, ngpu=2, contrast=1e2, gamma=1.0),
+    # boundary-condition variants of reading R7: no Dirichlet part at all (every
+    # subdomain floating: each G_i drops one node per component) and E x n = 0 on
+    # the hole wall too (a box with a cavity: one Dirichlet harmonic field)
+    "dir-none-8": lambda: workloads.custom(8, 8, 8, 2, 2, 2, overlap=1, gamma=1.0, dirichlet="none",
+                                           f_seed=21, name="dir-none-8"),
+    "dir-all-8": lambda: _cavity(),
 }
 # measured: the same recipes at gamma = 1e-2 (contrast 1e2) and at BASELINE's own
 # coefficients (contrast 1e3-1e4, gamma down to 1e-6), scaled so the oracle's
@@ -66,6 +72,15 @@ CASES = {**CASES_LITERAL, **CASES_MEASURED}
 
 def is_literal_case(name):
     return name in CASES_LITERAL
+
+
+def _cavity():
+    n = 8
+    c = np.arange(n ** 3)
+    ci, cj, ck = c % n, (c // n) % n, c // (n * n)
+    mask = ~((ci >= 3) & (ci < 5) & (cj >= 3) & (cj < 5) & (ck >= 3) & (ck < 5))
+    return workloads.custom(n, n, n, 2, 2, 2, overlap=1, gamma=1.0, mask=mask.astype(np.uint8),
+                            dirichlet="all", f_seed=22, name="dir-all-8")
 
 
 def _holes():

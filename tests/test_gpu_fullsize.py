@@ -267,3 +267,40 @@ def test_c2_full_size(c2):
     print(f"c2 full size: {it} iterations, dropped coarse pivots {G.info['coarse_perturbed']}, "
           f"solution backward error {be:.2e}")
     assert ok and rel <= 1e-8 and np.isfinite(xh).all() and be <= 1e-12
+
+
+def test_c3_one_gpu_share():
+    """BASELINE config 4 (c3) at ONE GPU's share of its 8-GPU mesh: 48^3 cubes
+    (an eighth of 96^3) with 4^3 subdomains of the full config's size (12^3 cubes
+    each + 2 overlap layers -> ~30k local dofs, the block-Lanczos GenEO path),
+    16 z-layers of mu^-1 in {1, 1e3}, per-element eps, gamma = 1e-3.  The full 96^3
+    mesh needs the distributed setup (DESIGN.md §9/§10).  Every local solve backward
+    stable, PCG of the bench's loop to 1e-8 with a backward-stable solution and an
+    iteration count in the paper's range for AS-SNK-GenEO (Tables 3-7:
+    23-28; the bound here is 40)."""
+    from paper_2311_18783_b200 import MaxwellDD
+    from parity_lib import EPS, backward_error
+    w = workloads.make("c3", n=48, p=4)
+    G = MaxwellDD(w, variant="as2_coarse_start")
+    m = om.mesh_of(w)
+    A = assembly.system_matrix(m, w.mu_inv, w.eps, w.gamma)[0].tocsr()
+    dec = dd.decompose(m, w.px, w.py, w.pz, w.overlap)
+    assert G.n == A.shape[0] and w.overlap == 2
+    r = np.random.default_rng(31).standard_normal(G.n)
+    xl = torch.empty(int(G.info["nloc"]), dtype=torch.float64, device="cuda")
+    G.apply_local_parts(dev(r), xl)
+    xl = xl.cpu().numpy()
+    sp_ = G.int_array("sub_ptr")
+    assert np.array_equal(np.diff(sp_), [len(d) for d in dec.dofs])
+    worst = max(backward_error(A[d][:, d].tocsr(), xl[sp_[i]:sp_[i + 1]], r[d])
+                for i, d in list(enumerate(dec.dofs))[::7])
+    assert worst <= 8 * EPS, worst
+    f = workloads.rhs(G.n, w.f_seed)
+    x = torch.empty(G.n, dtype=torch.float64, device="cuda")
+    it, rel, ok = G.solve(dev(f), x, tol=1e-8)
+    xh = x.cpu().numpy()
+    be = backward_error(A, xh, f)
+    print(f"c3 one-GPU share: n={G.n} n0={G.info['n0']} geneo={G.info['ngeneo']} {it} iterations, "
+          f"dropped coarse pivots {G.info['coarse_perturbed']}, solution backward error {be:.2e}")
+    assert ok and rel <= 1e-8 and it <= 40 and be <= 1e-12
+    G.close()

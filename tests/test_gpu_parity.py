@@ -81,7 +81,10 @@ def test_local_solves(name):
 @pytest.mark.parametrize("name", ALL)
 def test_coarse_solve_and_correction(name):
     m = measure_coarse(name)
-    assert m["coarse_bwd_gpu"] <= observed_tol(name, "coarse_bwd_gpu"), m
+    # the boundary-condition variants (dir-*) carry no recorded observation: a fixed
+    # 64 eps (the recorded literal cases observe 0.5e-15 .. 4.2e-15)
+    bwd_tol = observed_tol(name, "coarse_bwd_gpu") if name in OBSERVED else 64 * EPS
+    assert m["coarse_bwd_gpu"] <= bwd_tol, m
     if is_literal(name):
         assert m["coarse_vs_oracle"] <= 1e-10, m
     else:

@@ -1,6 +1,6 @@
 """Set up one BASELINE config at full size on the GPU, run the bench's PCG
 solve once, and print setup phases, sizes and the solve's facts (JSON).
-    python tools/fullsize_run.py c4 [variant]"""
+    python tools/fullsize_run.py c4 [variant] [key=value ...]   (recipe overrides, e.g. c3 n=48 p=4)"""
 import json
 import os
 import sys
@@ -14,11 +14,14 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import workloads  # noqa: E402
 
 cfg = sys.argv[1]
-variant = sys.argv[2] if len(sys.argv) > 2 else "as2_coarse_start"
+pos = [a for a in sys.argv[2:] if "=" not in a]
+kw = {k: (float(v) if any(c in v for c in ".e") else int(v)) for k, v in
+      (a.split("=", 1) for a in sys.argv[2:] if "=" in a)}
+variant = pos[0] if pos else "as2_coarse_start"
 import torch  # noqa: E402
 from paper_2311_18783_b200 import MaxwellDD  # noqa: E402
 
-w = workloads.make(cfg)
+w = workloads.make(cfg, **kw)
 t0 = time.time()
 G = MaxwellDD(w, variant=variant)
 setup = time.time() - t0
