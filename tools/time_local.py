@@ -14,7 +14,7 @@ from paper_2311_18783_b200 import MaxwellDD  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 w = workloads.make(cfg)
 ref = None
-for deal in sys.argv[2:] or ["snake", "lpt"]:
+for deal in [a for a in sys.argv[2:] if not a.startswith("-")] or ["snake", "lpt"]:
     os.environ["MDD_DEAL"] = deal
     G = MaxwellDD(w, coarse="none", variant="as1")
     st = torch.cuda.Stream()
@@ -35,4 +35,17 @@ for deal in sys.argv[2:] or ["snake", "lpt"]:
     if ref is None:
         ref = y.clone()
     print(json.dumps({"deal": deal, "local_ms": ms, "GBs": b / ms / 1e6, "bit_equal_to_first": same}), flush=True)
+    if os.environ.get("MDD_TRY_NOCOMPUTE"):   # experiment build (-DMDD_DEBUG_NOCOMPUTE): tiles streamed, no math
+        from paper_2311_18783_b200 import _lib
+        assert _lib.lib().mdd_debug_set_nocompute(1) == 0
+        for _ in range(3):
+            G.apply_local(v, y)
+        e0.record(st)
+        for _ in range(20):
+            G.apply_local(v, y)
+        e1.record(st)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        print(json.dumps({"deal": deal, "nocompute_local_ms": ms, "GBs": b / ms / 1e6}), flush=True)
+        assert _lib.lib().mdd_debug_set_nocompute(0) == 0
     G.close()
