@@ -96,11 +96,23 @@ enum { PH_GF = 0, PH_MF, PH_GB, PH_MB, PH_PR, PH_CF, PH_CB };
 // measured on c4: one CTA per combine item, coarse sweep 3.78 -> 3.65 ms)
 enum { SWF_NO_CTA_COMBINE = 2 };
 constexpr int kSweepThreads = 256;
-constexpr int kTileMax = 3328;   // doubles per tile (26 KB, one TMA bulk copy)
+// (MDD_TILE_MAX / MDD_SWEEP_CTAS: experiment builds through MDD_NVCC_FLAGS; measured on
+// c4's local sweep: 2304-double tiles with 4 CTAs per SM and 64 registers)
+#ifndef MDD_TILE_MAX
+#define MDD_TILE_MAX 3328
+#endif
+#ifndef MDD_SWEEP_CTAS
+#define MDD_SWEEP_CTAS 3
+#endif
+constexpr int kTileMax = MDD_TILE_MAX;   // doubles per tile (26 KB, one TMA bulk copy)
+constexpr int kSweepCtasPerSm = MDD_SWEEP_CTAS;  // resident persistent CTAs per SM (registers: launch bounds)
 constexpr int kVecMax = 512;     // rows of a small supernode / of a tile
 constexpr int64_t kSingleMax = 8192;    // stored entries of a supernode one CTA sweeps alone (measured: 32768 -> 8192 is -3 % per local sweep)
-constexpr int kStages = 2;       // tile ring slots per CTA (one tile streams while one computes)
-constexpr int kVecSlots = 3;     // task-vector slots (> the tasks the ring can span)
+#ifndef MDD_STAGES
+#define MDD_STAGES 2
+#endif
+constexpr int kStages = MDD_STAGES;       // tile ring slots per CTA (one tile streams while one computes)
+constexpr int kVecSlots = kStages + 1;    // task-vector slots (> the tasks the ring can span)
 constexpr int kDescAhead = 4;    // M-task descriptors streamed ahead of the current task
 constexpr int kDescRing = 8;     // descriptor ring slots (> kDescAhead)
 // MDD_SWEEP_TRACE words per (phase, CTA), thread 0's view (%globaltimer ns): start,

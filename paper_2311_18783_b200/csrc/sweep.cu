@@ -430,7 +430,7 @@ __device__ __forceinline__ void tile_matvec_t_packed(const double* T, int nr, in
 #endif
 }  // namespace
 
-__global__ void __launch_bounds__(kSweepThreads, 3) k_sweep(SweepDev S) {
+__global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(SweepDev S) {
   extern __shared__ __align__(128) double sm[];
   // kStages tile slots (a ring: kStages - 1 tiles stream while one is computed on),
   // kVecSlots task-vector slots, accumulators, reduction scratch

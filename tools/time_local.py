@@ -34,7 +34,8 @@ for deal in [a for a in sys.argv[2:] if not a.startswith("-")] or ["snake", "lpt
     same = None if ref is None else bool(torch.equal(ref, y))
     if ref is None:
         ref = y.clone()
-    print(json.dumps({"deal": deal, "local_ms": ms, "GBs": b / ms / 1e6, "bit_equal_to_first": same}), flush=True)
+    print(json.dumps({"deal": deal, "local_ms": ms, "GBs": b / ms / 1e6, "bit_equal_to_first": same,
+                      "ynorm": float(y.norm().item()), "grid": G.info.get("sweep_grid")}), flush=True)
     if os.environ.get("MDD_TRY_NOCOMPUTE"):   # experiment build (-DMDD_DEBUG_NOCOMPUTE): tiles streamed, no math
         from paper_2311_18783_b200 import _lib
         assert _lib.lib().mdd_debug_set_nocompute(1) == 0
