@@ -17,6 +17,10 @@ workload (weak scaling, no data-path collective: the sharded solve of sharded.cu
 replicates the setup and the coarse factor, so c4_weak64_xN does not fit it --
 DESIGN.md §9), value = all ranks' DOF*iterations / max-over-ranks time.
 
+--mode sharded: ONE copy of the workload with its subdomains sharded over the N
+ranks (strong scaling; halo exchanges and allreduces over NCCL, mdd_shard_solve);
+opt-in because no multi-GPU box was available to validate it beyond one rank.
+
 --impl reference times the CPU oracle (oracle/, fp64 numpy/scipy) on a bounded
 sample of the same recipe on rank 0; other ranks exit 0.
 """
