@@ -531,6 +531,20 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(SweepD
             const bool two = o + 32 < C.m;
             double a[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
             int q = q0;
+            // sixteen loads in flight per lane (the chains are dependent-latency
+            // bound: ~1 us per round); the same four chains in the same order
+            for (; q + 8 <= q1; q += 8) {
+              double t[8], u[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                t[k] = __ldcg(pb + (i64)(q + k) * C.ld + o);
+                u[k] = two ? __ldcg(pb + (i64)(q + k) * C.ld + o + 32) : 0.0;
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) { a[k] += t[k]; e[k] += u[k]; }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) { a[k] += t[k + 4]; e[k] += u[k + 4]; }
+            }
             for (; q + 4 <= q1; q += 4) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
@@ -566,6 +580,18 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(SweepD
           const bool two = o + 32 < C.m;
           double a[4] = {0.0, 0.0, 0.0, 0.0}, e[4] = {0.0, 0.0, 0.0, 0.0};
           int q = 0;
+          for (; q + 8 <= C.ntl; q += 8) {  // sixteen loads in flight, the same chains and order
+            double t[8], u[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              t[k] = __ldcg(pb + (i64)(q + k) * C.ld + o);
+              u[k] = two ? __ldcg(pb + (i64)(q + k) * C.ld + o + 32) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { a[k] += t[k]; e[k] += u[k]; }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) { a[k] += t[k + 4]; e[k] += u[k + 4]; }
+          }
           for (; q + 4 <= C.ntl; q += 4) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
