@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kSweepThreads, kSweepCtasPerSm) k_sweep(SweepD
     } else if (kind == PH_CF || kind == PH_CB) {
       // the partial sums of the level's 2-D row blocks (forward) / column blocks
       // (backward): one warp per block, each lane two outputs (o, o + 32) with four
-      // partial chains each (eight loads in flight); fixed order, grid-independent:
+      // partial chains each (sixteen loads in flight, two rounds of the four chains per trip); fixed order, grid-independent:
       // sum = (a0 + a1) + (a2 + a3), a_k = the partials q = k mod 4 in index order
       const bool cf = kind == PH_CF, fz = (PH.w & 1) != 0;
       const int lane = tid & 31;
